@@ -1,0 +1,130 @@
+/*
+ * bwm.h — C ABI of the B200-native BFAST-monitor hot path (libbwm.so).
+ *
+ * This is the drop-in boundary for the reference's fused batch backend:
+ *   breakwatch.engine._fused_phases   (reference pkg/src/breakwatch/engine.py:322-411)
+ * plus the two compiled kernels it calls,
+ *   breakwatch._kernels.mosum_block   (reference pkg/src/breakwatch/_kernels.py:21-34)
+ *   breakwatch._kernels.detect_block  (reference pkg/src/breakwatch/_kernels.py:37-48)
+ * and the gap-fill ingest it runs first,
+ *   breakwatch.engine._ingest_block   (reference pkg/src/breakwatch/engine.py:305-319).
+ *
+ * One call = one fused pass per pixel: forward/back gap fill -> beta = M . y_hist
+ * -> residuals -> sigma -> sliding MOSUM -> strict boundary test -> first break,
+ * max |MO| (and optionally beta, the MOSUM mean, the full MOSUM matrix).
+ *
+ * Conventions (mirroring the reference kernel seam, _kernels.py:21,37):
+ *   - all arrays are caller-allocated; the hot call (bwm_monitor) never allocates;
+ *   - data is time-major: y[t * ld_y + pixel], float32, NaN/+-Inf = missing;
+ *   - outputs are per pixel, written at out[pixel] (beta/mosum: out[row * ld_out + pixel]);
+ *   - return 0 on success, a negative BWM_E* code for invalid arguments, or a positive
+ *     cudaError_t value for CUDA failures; bwm_last_error() holds the message (per thread).
+ *
+ * The constant tables (mapping, design, boundary) are host setup in float64 — exactly
+ * the reference's build_design_matrix / fit_mapping / boundary_values
+ * (model.py:90-152, mosum.py:68-79) — and are handed over once through bwm_plan_create.
+ */
+#ifndef BWM_H
+#define BWM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BWM_ABI_VERSION 1
+
+/* error codes (negative); positive returns are cudaError_t values */
+#define BWM_OK 0
+#define BWM_E_NULL (-1)        /* required pointer is NULL                      */
+#define BWM_E_DIMS (-2)        /* inconsistent dimensions (n >= N, h > n, ...)  */
+#define BWM_E_PARAMS (-3)      /* n_params outside the compiled set {4,...,18}  */
+#define BWM_E_SMEM (-4)        /* tables + MOSUM ring exceed shared memory      */
+#define BWM_E_DEVICE (-5)      /* plan used on a different device               */
+#define BWM_E_ZERO_SIGMA (-6)  /* not returned by bwm_monitor; see zero_sigma   */
+
+/* Geometry shared by every pixel of a batch (reference MonitorConfig, engine.py:102-134). */
+typedef struct bwm_dims {
+    int32_t n_obs;      /* N : observations per series (rows of the stack)          */
+    int32_t n_hist;     /* n : stable history length, p < n < N                     */
+    int32_t bandwidth;  /* h : MOSUM window (integer count), 1 <= h <= n            */
+    int32_t n_params;   /* p = 2 + 2k : intercept, trend, k sin/cos pairs           */
+} bwm_dims;
+
+/*
+ * Host-side float64 constants for one batch geometry.  The kernel runs in a
+ * re-centred but equivalent basis: the trend regressor t is replaced by
+ * (t - trend_center) / trend_scale, which leaves fitted values, residuals and
+ * MOSUM unchanged in exact arithmetic and keeps the float32 contraction well
+ * conditioned.  Beta is reported back in the reference's raw basis.
+ */
+typedef struct bwm_tables {
+    const double* mapping;   /* [p][n]  M' = (X'_h X'_h^T)^-1 X'_h (centred basis)         */
+    const double* design;    /* [p][N]  X'  rows: 1, (t-tc)/ts, sin(2pi j t/f), cos(...)    */
+    const double* bound;     /* [N-n]   crit * sqrt(log_plus((n+1+j)/n))  (mosum.py:68-79)  */
+    double trend_center;     /* tc */
+    double trend_scale;      /* ts */
+} bwm_tables;
+
+/* Per-pixel outputs.  Required: valid, first_idx, max_abs.  Optional: NULL to skip. */
+typedef struct bwm_outputs {
+    uint8_t* valid;          /* [P]  1 if the series has a finite sample (engine.py:308)          */
+    int32_t* first_idx;      /* [P]  0 = no break, else 1-based offset into the monitor period    */
+    float* max_abs;          /* [P]  max_j |MO_j|                                                  */
+    float* beta;             /* [p][ld_out] or NULL: history coefficients, raw basis (model.py:90) */
+    float* mo_mean;          /* [P] or NULL: mean_j MO_j                                           */
+    float* mosum;            /* [N-n][ld_out] or NULL: the MOSUM process (keep_mosum)              */
+    int64_t ld_out;          /* leading dimension of beta / mosum (>= P)                           */
+    /* lowest global pixel index whose history fits exactly (sigma == 0); caller initialises
+       to INT64_MAX (device pointer for bwm_monitor, host pointer for bwm_monitor_host).
+       Mirrors ZeroResidualError (engine.py:373-378). */
+    int64_t* zero_sigma_pixel;
+} bwm_outputs;
+
+typedef struct bwm_plan bwm_plan;
+
+/* Build the device-resident constant tables on `device` (cudaSetDevice is restored). */
+int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tables, int device,
+                    bwm_plan** out_plan);
+void bwm_plan_destroy(bwm_plan* plan);
+
+/*
+ * Hot call, device pointers, asynchronous on `stream` (a cudaStream_t; NULL = legacy).
+ *   y        : device float32 [N][ld_y], pixel p of this shard at column p
+ *   n_pixels : pixels in this shard (P)
+ *   pixel_offset : global index of this shard's pixel 0 (for zero_sigma_pixel)
+ * No allocation, no synchronisation.  Re-entrant across streams and devices.
+ */
+int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pixels,
+                int64_t pixel_offset, const bwm_outputs* out, void* stream);
+
+/*
+ * End-to-end call with HOST buffers (the reference-facing path: a numpy stack in,
+ * numpy maps out).  Pixels are processed in column chunks; the H2D copy of chunk
+ * i+1 overlaps the kernel of chunk i and the D2H of chunk i-1 on separate streams.
+ * y_host may be pageable or pinned (pinned is faster).  Blocks until done.
+ * Outputs are host pointers with the same layout as bwm_outputs.
+ */
+int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t n_pixels,
+                     int64_t pixel_offset, const bwm_outputs* out_host);
+
+/* Kernel time (ms) of the last bwm_monitor_host call, summed over chunks; and its
+   H2D/D2H byte counts.  For PhaseTimings. */
+int bwm_last_host_stats(const bwm_plan* plan, double* kernel_ms, double* total_ms,
+                        int64_t* h2d_bytes, int64_t* d2h_bytes);
+
+/* Number of bwm kernel launches issued by this process so far (all plans). */
+int64_t bwm_launch_count(void);
+
+/* Shared memory (bytes) a launch with these dims needs; <0 if unsupported. */
+int64_t bwm_smem_bytes(const bwm_dims* dims);
+
+const char* bwm_last_error(void);
+int bwm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BWM_H */

@@ -1,0 +1,116 @@
+"""ctypes binding of libbwm.so (the C ABI declared in include/bwm.h).
+
+The library is built in-tree (``paper_1807_01751_b200/libbwm.so``, see build.py).  There
+is deliberately no fallback: if the library or a CUDA device is missing, every entry
+point raises.  Structs mirror include/bwm.h field for field.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libbwm.so"
+
+BWM_OK = 0
+BWM_E_NULL = -1
+BWM_E_DIMS = -2
+BWM_E_PARAMS = -3
+BWM_E_SMEM = -4
+BWM_E_DEVICE = -5
+
+INT64_MAX = (1 << 63) - 1
+
+
+class Dims(C.Structure):
+    _fields_ = [
+        ("n_obs", C.c_int32),
+        ("n_hist", C.c_int32),
+        ("bandwidth", C.c_int32),
+        ("n_params", C.c_int32),
+    ]
+
+
+class Tables(C.Structure):
+    _fields_ = [
+        ("mapping", C.POINTER(C.c_double)),
+        ("design", C.POINTER(C.c_double)),
+        ("bound", C.POINTER(C.c_double)),
+        ("trend_center", C.c_double),
+        ("trend_scale", C.c_double),
+    ]
+
+
+class Outputs(C.Structure):
+    _fields_ = [
+        ("valid", C.c_void_p),
+        ("first_idx", C.c_void_p),
+        ("max_abs", C.c_void_p),
+        ("beta", C.c_void_p),
+        ("mo_mean", C.c_void_p),
+        ("mosum", C.c_void_p),
+        ("ld_out", C.c_int64),
+        ("zero_sigma_pixel", C.c_void_p),
+    ]
+
+
+# (name, restype, argtypes) — every symbol include/bwm.h declares
+SIGNATURES = [
+    ("bwm_plan_create", C.c_int, [C.POINTER(Dims), C.POINTER(Tables), C.c_int, C.POINTER(C.c_void_p)]),
+    ("bwm_plan_destroy", None, [C.c_void_p]),
+    ("bwm_monitor", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Outputs), C.c_void_p]),
+    ("bwm_monitor_host", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Outputs)]),
+    ("bwm_last_host_stats", C.c_int,
+     [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("bwm_launch_count", C.c_int64, []),
+    ("bwm_smem_bytes", C.c_int64, [C.POINTER(Dims)]),
+    ("bwm_last_error", C.c_char_p, []),
+    ("bwm_abi_version", C.c_int, []),
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libbwm.so (once).  Raises if it has not been built — no CPU fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("BWM_LIB", LIB_PATH))
+    if not path.exists():
+        raise RuntimeError(
+            f"libbwm.so not found at {path}; build it with "
+            "`python -m paper_1807_01751_b200.build` (there is no CPU fallback)"
+        )
+    lib = C.CDLL(str(path))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.bwm_abi_version() != 1:
+        raise RuntimeError("libbwm ABI version mismatch; rebuild the library")
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().bwm_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    """Map a libbwm return code onto the reference's exception types."""
+    if rc == BWM_OK:
+        return
+    from .errors import DeviceError
+
+    msg = f"{what}: {last_error()}"
+    if rc in (BWM_E_DIMS, BWM_E_NULL, BWM_E_PARAMS):
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+def launch_count() -> int:
+    return int(load().bwm_launch_count())

@@ -1,0 +1,529 @@
+// bwm_capi.cu — C ABI of libbwm.so (declared in include/bwm.h).
+//
+// Owns: the device-resident constant tables (bwm_plan), kernel dispatch over the
+// compiled (n_params, vectorised, ring) variants, persistent-grid sizing, and the
+// host-buffer pipeline (bwm_monitor_host) that streams pixel chunks through the GPU
+// with H2D / kernel / D2H overlapped on separate streams.
+#include "../../include/bwm.h"
+#include "bwm_variants.cuh"
+
+#include <atomic>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#define BWM_DECLARE_PICK(NP) bwm::KernelFn bwm_pick_p##NP(int kind, bool ring);
+// per-n_params kernel tables, one translation unit each (bwm_variants_p*.cu)
+BWM_DECLARE_PICK(4)
+BWM_DECLARE_PICK(6)
+BWM_DECLARE_PICK(8)
+BWM_DECLARE_PICK(10)
+BWM_DECLARE_PICK(12)
+BWM_DECLARE_PICK(14)
+BWM_DECLARE_PICK(16)
+BWM_DECLARE_PICK(18)
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int set_err(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define BWM_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return set_err((int)e_, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                           __FILE__, __LINE__);                                        \
+    } while (0)
+
+constexpr int kRingMaxH = 64;   // ring in smem up to h = 64 (64 KB); above: lagging cursor
+
+// shared memory of the LDG kernel: tables + MOSUM ring
+int64_t smem_bytes_for(int N, int n, int h, int p, bool ring) {
+    const int sp = (p + 3) & ~3;
+    int64_t fl = (int64_t)n * sp + (int64_t)N * sp + (((N - n) + 3) & ~3);
+    int64_t bytes = fl * 4;
+    if (ring) bytes += (int64_t)h * bwm::kThreads * 8;
+    return bytes;
+}
+
+// shared memory of the TMA kernel: stage ring + the above + 2*kStages mbarriers
+int64_t smem_bytes_tma(int N, int n, int h, int p, bool ring) {
+    return bwm::kStages * bwm::tma_stage_bytes(ring) + smem_bytes_for(N, n, h, p, ring) +
+           2 * bwm::kStages * 8;
+}
+
+using bwm::Kind;
+using bwm::kLdgFast;
+using bwm::kLdgSafe;
+using bwm::kTma;
+using bwm::KernelFn;
+
+struct DeviceRestore {
+    int prev = -1;
+    explicit DeviceRestore(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceRestore() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// (n_params, kind, ring) -> kernel.  kLdgSafe: tail tile / misaligned input (scalar loads).
+KernelFn pick(int p, Kind kind, bool ring) {
+    switch (p) {
+        case 4: return bwm_pick_p4(kind, ring);
+        case 6: return bwm_pick_p6(kind, ring);
+        case 8: return bwm_pick_p8(kind, ring);
+        case 10: return bwm_pick_p10(kind, ring);
+        case 12: return bwm_pick_p12(kind, ring);
+        case 14: return bwm_pick_p14(kind, ring);
+        case 16: return bwm_pick_p16(kind, ring);
+        case 18: return bwm_pick_p18(kind, ring);
+        default: return nullptr;
+    }
+}
+
+int threads_of(Kind k) { return k == kTma ? bwm::kTmaThreads : bwm::kThreads; }
+
+}  // namespace
+
+struct HostPipe {
+    int64_t chunk = 0;                 // pixels per chunk
+    int nbuf = 0;
+    float* d_y[2] = {nullptr, nullptr};
+    uint8_t* d_valid[2] = {nullptr, nullptr};
+    int32_t* d_first[2] = {nullptr, nullptr};
+    float* d_max[2] = {nullptr, nullptr};
+    float* d_beta[2] = {nullptr, nullptr};
+    float* d_mean[2] = {nullptr, nullptr};
+    float* d_mosum[2] = {nullptr, nullptr};
+    int64_t* d_zero = nullptr;         // [2]
+    cudaStream_t s_h2d[2] = {nullptr, nullptr};
+    cudaStream_t s_k[2] = {nullptr, nullptr};
+    cudaEvent_t ev_in[2], ev_k0[2], ev_k1[2], ev_free[2];
+    bool events = false;
+    double last_kernel_ms = 0, last_total_ms = 0;
+    int64_t last_h2d = 0, last_d2h = 0;
+};
+
+struct bwm_plan {
+    bwm_dims dims{};
+    int device = 0;
+    int sp = 0;
+    float* d_mt = nullptr;
+    float* d_xt = nullptr;
+    float* d_bound = nullptr;
+    float inv_dof = 0, sqrt_n = 0, tc_ts = 0, inv_ts = 0;
+    bool ring = true;
+    int64_t smem = 0;                  // LDG kernels
+    int64_t smem_tma = 0;              // TMA kernel (0: does not fit -> LDG kernels only)
+    int sms = 0;
+    int blocks_per_sm[3] = {0, 0, 0};  // [Kind]
+    bool force_ldg = false;            // BWM_KERNEL=ldg (A/B against the TMA kernel)
+    HostPipe pipe;
+    std::mutex mu;                     // serialises bwm_monitor_host on one plan
+};
+
+static int validate_dims(const bwm_dims* d) {
+    if (!d) return set_err(BWM_E_NULL, "dims is NULL");
+    if (d->n_params < 4 || d->n_params > 18 || (d->n_params & 1))
+        return set_err(BWM_E_PARAMS, "n_params=%d not in {4,6,...,18} (harmonics 1..8)", d->n_params);
+    if (!(d->n_hist > d->n_params))
+        return set_err(BWM_E_DIMS, "history must exceed the coefficient count (n=%d, p=%d)",
+                       d->n_hist, d->n_params);
+    if (!(d->n_hist < d->n_obs))
+        return set_err(BWM_E_DIMS, "history must end before the series does (n=%d, N=%d)",
+                       d->n_hist, d->n_obs);
+    if (d->bandwidth < 1 || d->bandwidth > d->n_hist)
+        return set_err(BWM_E_DIMS, "bandwidth must satisfy 1 <= h <= n (h=%d, n=%d)", d->bandwidth,
+                       d->n_hist);
+    return BWM_OK;
+}
+
+extern "C" {
+
+const char* bwm_last_error(void) { return g_err.c_str(); }
+int bwm_abi_version(void) { return BWM_ABI_VERSION; }
+int64_t bwm_launch_count(void) { return g_launches.load(); }
+
+int64_t bwm_smem_bytes(const bwm_dims* d) {
+    int rc = validate_dims(d);
+    if (rc) return rc;
+    const bool ring = d->bandwidth <= kRingMaxH;
+    return smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, ring);
+}
+
+int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_plan** out_plan) {
+    if (!out_plan) return set_err(BWM_E_NULL, "out_plan is NULL");
+    *out_plan = nullptr;
+    int rc = validate_dims(dims);
+    if (rc) return rc;
+    if (!tb || !tb->mapping || !tb->design || !tb->bound)
+        return set_err(BWM_E_NULL, "tables (mapping, design, bound) must be non-NULL");
+    if (!(tb->trend_scale > 0) || !std::isfinite(tb->trend_center))
+        return set_err(BWM_E_DIMS, "trend_scale must be positive and trend_center finite");
+
+    DeviceRestore guard(device);
+    BWM_CUDA(cudaSetDevice(device));
+    const int N = dims->n_obs, n = dims->n_hist, p = dims->n_params, h = dims->bandwidth;
+    const int sp = (p + 3) & ~3;
+
+    auto* plan = new bwm_plan();
+    plan->dims = *dims;
+    plan->device = device;
+    plan->sp = sp;
+    plan->ring = h <= kRingMaxH;
+    plan->smem = smem_bytes_for(N, n, h, p, plan->ring);
+    plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->ring);
+    const char* env = getenv("BWM_KERNEL");
+    plan->force_ldg = env && strcmp(env, "ldg") == 0;
+    plan->inv_dof = (float)(1.0 / (double)(n - p));
+    plan->sqrt_n = (float)std::sqrt((double)n);
+    plan->tc_ts = (float)(tb->trend_center / tb->trend_scale);
+    plan->inv_ts = (float)(1.0 / tb->trend_scale);
+
+    int max_optin = 0;
+    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device);
+    if (plan->smem_tma > max_optin) plan->smem_tma = 0;
+    if (plan->smem > max_optin) {
+        int64_t need = plan->smem;
+        delete plan;
+        return set_err(BWM_E_SMEM, "tables need %lld B of shared memory, device allows %d",
+                       (long long)need, max_optin);
+    }
+
+    // float32 tables, transposed so one date's coefficients are contiguous (LDS.128)
+    std::vector<float> mt((size_t)n * sp, 0.f), xt((size_t)N * sp, 0.f), bd((size_t)(N - n));
+    for (int i = 0; i < p; ++i) {
+        for (int t = 0; t < n; ++t) mt[(size_t)t * sp + i] = (float)tb->mapping[(size_t)i * n + t];
+        for (int t = 0; t < N; ++t) xt[(size_t)t * sp + i] = (float)tb->design[(size_t)i * N + t];
+    }
+    for (int j = 0; j < N - n; ++j) bd[j] = (float)tb->bound[j];
+
+    auto fail = [&](cudaError_t e, const char* what) {
+        cudaFree(plan->d_mt);
+        cudaFree(plan->d_xt);
+        cudaFree(plan->d_bound);
+        delete plan;
+        return set_err((int)e, "%s: %s", what, cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&plan->d_mt, mt.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&plan->d_xt, xt.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&plan->d_bound, std::max<size_t>(bd.size(), 1) * 4)) != cudaSuccess)
+        return fail(e, "cudaMalloc");
+    if ((e = cudaMemcpy(plan->d_mt, mt.data(), mt.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy");
+    if ((e = cudaMemcpy(plan->d_xt, xt.data(), xt.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy");
+    if ((e = cudaMemcpy(plan->d_bound, bd.data(), bd.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy");
+
+    for (int v = 0; v < 3; ++v) {
+        const Kind kind = (Kind)v;
+        const int64_t sm = kind == kTma ? plan->smem_tma : plan->smem;
+        if (kind == kTma && sm == 0) continue;
+        KernelFn fn = pick(p, kind, plan->ring);
+        if ((e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sm)) != cudaSuccess)
+            return fail(e, "cudaFuncSetAttribute");
+        int nb = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, threads_of(kind),
+                                                               (size_t)sm)) != cudaSuccess)
+            return fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+        plan->blocks_per_sm[v] = std::max(nb, 1);
+    }
+    *out_plan = plan;
+    return BWM_OK;
+}
+
+static void pipe_free(HostPipe& hp) {
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(hp.d_y[b]);
+        cudaFree(hp.d_valid[b]);
+        cudaFree(hp.d_first[b]);
+        cudaFree(hp.d_max[b]);
+        cudaFree(hp.d_beta[b]);
+        cudaFree(hp.d_mean[b]);
+        cudaFree(hp.d_mosum[b]);
+        if (hp.s_h2d[b]) cudaStreamDestroy(hp.s_h2d[b]);
+        if (hp.s_k[b]) cudaStreamDestroy(hp.s_k[b]);
+        if (hp.events) {
+            cudaEventDestroy(hp.ev_in[b]);
+            cudaEventDestroy(hp.ev_k0[b]);
+            cudaEventDestroy(hp.ev_k1[b]);
+            cudaEventDestroy(hp.ev_free[b]);
+        }
+    }
+    cudaFree(hp.d_zero);
+    hp = HostPipe();
+}
+
+void bwm_plan_destroy(bwm_plan* plan) {
+    if (!plan) return;
+    DeviceRestore guard(plan->device);
+    cudaSetDevice(plan->device);
+    pipe_free(plan->pipe);
+    cudaFree(plan->d_mt);
+    cudaFree(plan->d_xt);
+    cudaFree(plan->d_bound);
+    delete plan;
+}
+
+int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pixels,
+                int64_t pixel_offset, const bwm_outputs* out, void* stream) {
+    if (!plan) return set_err(BWM_E_NULL, "plan is NULL");
+    if (!y || !out || !out->valid || !out->first_idx || !out->max_abs || !out->zero_sigma_pixel)
+        return set_err(BWM_E_NULL, "y and outputs valid/first_idx/max_abs/zero_sigma_pixel are required");
+    if (n_pixels < 1) return set_err(BWM_E_DIMS, "stack needs at least one pixel");
+    if (ld_y < n_pixels) return set_err(BWM_E_DIMS, "ld_y (%lld) < n_pixels (%lld)", (long long)ld_y,
+                                        (long long)n_pixels);
+    if ((out->beta || out->mosum) && out->ld_out < n_pixels)
+        return set_err(BWM_E_DIMS, "ld_out (%lld) < n_pixels (%lld)", (long long)out->ld_out,
+                       (long long)n_pixels);
+    if (pixel_offset < 0) return set_err(BWM_E_DIMS, "pixel_offset must be >= 0");
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != plan->device)
+        return set_err(BWM_E_DEVICE, "plan lives on device %d, current device is %d", plan->device, cur);
+
+    const bwm_dims& d = plan->dims;
+    bwm::KParams k{};
+    k.y = y;
+    k.ld_y = ld_y;
+    k.n_pixels = n_pixels;
+    k.pixel_offset = pixel_offset;
+    k.N = d.n_obs;
+    k.n = d.n_hist;
+    k.h = d.bandwidth;
+    k.sp = plan->sp;
+    k.mt = plan->d_mt;
+    k.xt = plan->d_xt;
+    k.bound = plan->d_bound;
+    k.inv_dof = plan->inv_dof;
+    k.sqrt_n = plan->sqrt_n;
+    k.tc_ts = plan->tc_ts;
+    k.inv_ts = plan->inv_ts;
+    k.valid = out->valid;
+    k.first_idx = out->first_idx;
+    k.max_abs = out->max_abs;
+    k.beta = out->beta;
+    k.mo_mean = out->mo_mean;
+    k.mosum = out->mosum;
+    k.ld_out = out->ld_out;
+    k.zero_sigma = reinterpret_cast<unsigned long long*>(out->zero_sigma_pixel);
+
+    // Whole 256-pixel tiles go to the TMA kernel (rows 16-byte aligned, outputs 8-byte
+    // aligned) or, with BWM_KERNEL=ldg / when its smem does not fit, the LDG fast kernel
+    // (rows 8-byte aligned); the tail tile, or everything when misaligned, goes to the
+    // scalar bounds-checked LDG kernel.
+    auto al = [](const void* q, uintptr_t a) { return (reinterpret_cast<uintptr_t>(q) & (a - 1)) == 0; };
+    const bool out_al = al(out->valid, 2) && al(out->first_idx, 8) && al(out->max_abs, 8) &&
+                        (!out->mo_mean || al(out->mo_mean, 8)) && (!out->beta || al(out->beta, 8)) &&
+                        (!out->mosum || al(out->mosum, 8)) && (out->ld_out % 2 == 0 || (!out->beta && !out->mosum));
+    const bool tma_ok = !plan->force_ldg && plan->smem_tma > 0 && al(y, 16) && (ld_y % 4 == 0) && out_al;
+    const bool ldg_ok = al(y, 8) && (ld_y % 2 == 0);
+    const Kind main_kind = tma_ok ? kTma : kLdgFast;
+    const int64_t full = (tma_ok || ldg_ok) ? (n_pixels / bwm::kTile) * bwm::kTile : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    int launched = 0;
+    for (int part = 0; part < 2; ++part) {
+        const Kind kind = part == 0 ? main_kind : kLdgSafe;
+        const int64_t p0 = part == 0 ? 0 : full;
+        const int64_t cnt = part == 0 ? full : n_pixels - full;
+        if (cnt <= 0) continue;
+        bwm::KParams kp = k;
+        kp.y = y + p0;
+        kp.n_pixels = cnt;
+        kp.pixel_offset = pixel_offset + p0;
+        kp.valid = out->valid + p0;
+        kp.first_idx = out->first_idx + p0;
+        kp.max_abs = out->max_abs + p0;
+        kp.beta = out->beta ? out->beta + p0 : nullptr;
+        kp.mo_mean = out->mo_mean ? out->mo_mean + p0 : nullptr;
+        kp.mosum = out->mosum ? out->mosum + p0 : nullptr;
+        KernelFn fn = pick(d.n_params, kind, plan->ring);
+        const int64_t tiles = (cnt + bwm::kTile - 1) / bwm::kTile;
+        const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * plan->blocks_per_sm[kind]);
+        const size_t sm = (size_t)(kind == kTma ? plan->smem_tma : plan->smem);
+        fn<<<(unsigned)grid, threads_of(kind), sm, st>>>(kp);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
+        ++launched;
+    }
+    g_launches.fetch_add(launched);
+    return BWM_OK;
+}
+
+static int pipe_ensure(bwm_plan* plan, int64_t chunk, bool beta, bool mean, bool mosum) {
+    HostPipe& hp = plan->pipe;
+    const bwm_dims& d = plan->dims;
+    const bool need_realloc = hp.chunk != chunk || (beta && !hp.d_beta[0]) || (mean && !hp.d_mean[0]) ||
+                              (mosum && !hp.d_mosum[0]);
+    if (!need_realloc) return BWM_OK;
+    pipe_free(hp);
+    hp.chunk = chunk;
+    hp.nbuf = 2;
+    for (int b = 0; b < 2; ++b) {
+        BWM_CUDA(cudaMalloc(&hp.d_y[b], (size_t)d.n_obs * chunk * 4));
+        BWM_CUDA(cudaMalloc(&hp.d_valid[b], (size_t)chunk));
+        BWM_CUDA(cudaMalloc(&hp.d_first[b], (size_t)chunk * 4));
+        BWM_CUDA(cudaMalloc(&hp.d_max[b], (size_t)chunk * 4));
+        if (beta) BWM_CUDA(cudaMalloc(&hp.d_beta[b], (size_t)d.n_params * chunk * 4));
+        if (mean) BWM_CUDA(cudaMalloc(&hp.d_mean[b], (size_t)chunk * 4));
+        if (mosum) BWM_CUDA(cudaMalloc(&hp.d_mosum[b], (size_t)(d.n_obs - d.n_hist) * chunk * 4));
+        BWM_CUDA(cudaStreamCreateWithFlags(&hp.s_h2d[b], cudaStreamNonBlocking));
+        BWM_CUDA(cudaStreamCreateWithFlags(&hp.s_k[b], cudaStreamNonBlocking));
+        BWM_CUDA(cudaEventCreateWithFlags(&hp.ev_in[b], cudaEventDisableTiming));
+        BWM_CUDA(cudaEventCreate(&hp.ev_k0[b]));
+        BWM_CUDA(cudaEventCreate(&hp.ev_k1[b]));
+        BWM_CUDA(cudaEventCreateWithFlags(&hp.ev_free[b], cudaEventDisableTiming));
+    }
+    hp.events = true;
+    BWM_CUDA(cudaMalloc(&hp.d_zero, 2 * sizeof(int64_t)));
+    return BWM_OK;
+}
+
+int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t n_pixels,
+                     int64_t pixel_offset, const bwm_outputs* out) {
+    if (!plan) return set_err(BWM_E_NULL, "plan is NULL");
+    if (!y_host || !out || !out->valid || !out->first_idx || !out->max_abs || !out->zero_sigma_pixel)
+        return set_err(BWM_E_NULL, "y and outputs valid/first_idx/max_abs/zero_sigma_pixel are required");
+    if (n_pixels < 1) return set_err(BWM_E_DIMS, "stack needs at least one pixel");
+    if (ld_y < n_pixels) return set_err(BWM_E_DIMS, "ld_y < n_pixels");
+    if ((out->beta || out->mosum) && out->ld_out < n_pixels) return set_err(BWM_E_DIMS, "ld_out < n_pixels");
+
+    std::lock_guard<std::mutex> lock(plan->mu);
+    DeviceRestore guard(plan->device);
+    BWM_CUDA(cudaSetDevice(plan->device));
+    const bwm_dims& d = plan->dims;
+    const int N = d.n_obs, M = d.n_obs - d.n_hist, p = d.n_params;
+
+    // chunk: ~512 MB of y per buffer, multiple of the CTA tile
+    int64_t chunk = (512ll << 20) / (4ll * N);
+    chunk = std::max<int64_t>(bwm::kTile, (chunk / bwm::kTile) * bwm::kTile);
+    if (chunk >= n_pixels) chunk = ((n_pixels + bwm::kTile - 1) / bwm::kTile) * bwm::kTile;
+    int rc = pipe_ensure(plan, chunk, out->beta != nullptr, out->mo_mean != nullptr, out->mosum != nullptr);
+    if (rc) return rc;
+    HostPipe& hp = plan->pipe;
+
+    const int64_t init[2] = {INT64_MAX, INT64_MAX};
+    BWM_CUDA(cudaMemcpy(hp.d_zero, init, sizeof init, cudaMemcpyHostToDevice));
+
+    cudaEvent_t t_start, t_end;
+    BWM_CUDA(cudaEventCreate(&t_start));
+    BWM_CUDA(cudaEventCreate(&t_end));
+    BWM_CUDA(cudaEventRecord(t_start, hp.s_h2d[0]));
+    BWM_CUDA(cudaStreamWaitEvent(hp.s_h2d[1], t_start, 0));
+
+    const int64_t n_chunks = (n_pixels + chunk - 1) / chunk;
+    int64_t h2d = 0, d2h = 0;
+    std::vector<cudaEvent_t> kev((size_t)(2 * n_chunks), nullptr);   // per-chunk kernel timing
+    for (auto& ev : kev) BWM_CUDA(cudaEventCreate(&ev));
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        const int b = (int)(c & 1);
+        const int64_t p0 = c * chunk;
+        const int64_t w = std::min(chunk, n_pixels - p0);
+        // buffer b is free once chunk c-2 finished its D2H
+        if (c >= 2) BWM_CUDA(cudaStreamWaitEvent(hp.s_h2d[b], hp.ev_free[b], 0));
+        BWM_CUDA(cudaMemcpy2DAsync(hp.d_y[b], (size_t)w * 4, y_host + p0, (size_t)ld_y * 4,
+                                   (size_t)w * 4, (size_t)N, cudaMemcpyHostToDevice, hp.s_h2d[b]));
+        h2d += (int64_t)w * 4 * N;
+        BWM_CUDA(cudaEventRecord(hp.ev_in[b], hp.s_h2d[b]));
+        BWM_CUDA(cudaStreamWaitEvent(hp.s_k[b], hp.ev_in[b], 0));
+        bwm_outputs o{};
+        o.valid = hp.d_valid[b];
+        o.first_idx = hp.d_first[b];
+        o.max_abs = hp.d_max[b];
+        o.beta = out->beta ? hp.d_beta[b] : nullptr;
+        o.mo_mean = out->mo_mean ? hp.d_mean[b] : nullptr;
+        o.mosum = out->mosum ? hp.d_mosum[b] : nullptr;
+        o.ld_out = w;
+        o.zero_sigma_pixel = hp.d_zero + b;
+        BWM_CUDA(cudaEventRecord(kev[2 * c], hp.s_k[b]));
+        rc = bwm_monitor(plan, hp.d_y[b], w, w, pixel_offset + p0, &o, hp.s_k[b]);
+        if (rc) return rc;
+        BWM_CUDA(cudaEventRecord(kev[2 * c + 1], hp.s_k[b]));
+        cudaStream_t s = hp.s_k[b];
+        BWM_CUDA(cudaMemcpyAsync(out->valid + p0, hp.d_valid[b], (size_t)w, cudaMemcpyDeviceToHost, s));
+        BWM_CUDA(cudaMemcpyAsync(out->first_idx + p0, hp.d_first[b], (size_t)w * 4, cudaMemcpyDeviceToHost, s));
+        BWM_CUDA(cudaMemcpyAsync(out->max_abs + p0, hp.d_max[b], (size_t)w * 4, cudaMemcpyDeviceToHost, s));
+        d2h += w * 9;
+        if (out->mo_mean) {
+            BWM_CUDA(cudaMemcpyAsync(out->mo_mean + p0, hp.d_mean[b], (size_t)w * 4, cudaMemcpyDeviceToHost, s));
+            d2h += w * 4;
+        }
+        if (out->beta) {
+            BWM_CUDA(cudaMemcpy2DAsync(out->beta + p0, (size_t)out->ld_out * 4, hp.d_beta[b], (size_t)w * 4,
+                                       (size_t)w * 4, (size_t)p, cudaMemcpyDeviceToHost, s));
+            d2h += w * 4 * p;
+        }
+        if (out->mosum) {
+            BWM_CUDA(cudaMemcpy2DAsync(out->mosum + p0, (size_t)out->ld_out * 4, hp.d_mosum[b], (size_t)w * 4,
+                                       (size_t)w * 4, (size_t)M, cudaMemcpyDeviceToHost, s));
+            d2h += w * 4 * M;
+        }
+        BWM_CUDA(cudaEventRecord(hp.ev_free[b], s));
+    }
+    double kernel_ms = 0;
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        BWM_CUDA(cudaEventSynchronize(kev[2 * c + 1]));
+        float ms = 0;
+        BWM_CUDA(cudaEventElapsedTime(&ms, kev[2 * c], kev[2 * c + 1]));
+        kernel_ms += ms;
+    }
+    for (auto& ev : kev) cudaEventDestroy(ev);
+    for (int b = 0; b < 2; ++b) {
+        BWM_CUDA(cudaStreamSynchronize(hp.s_k[b]));
+        BWM_CUDA(cudaStreamSynchronize(hp.s_h2d[b]));
+    }
+    int64_t z[2];
+    BWM_CUDA(cudaMemcpy(z, hp.d_zero, sizeof z, cudaMemcpyDeviceToHost));
+    d2h += sizeof z;
+    const int64_t zmin = std::min(z[0], z[1]);
+    if (zmin < *out->zero_sigma_pixel) *out->zero_sigma_pixel = zmin;
+    BWM_CUDA(cudaEventRecord(t_end, hp.s_k[0]));
+    BWM_CUDA(cudaEventSynchronize(t_end));
+    float total = 0;
+    cudaEventElapsedTime(&total, t_start, t_end);
+    cudaEventDestroy(t_start);
+    cudaEventDestroy(t_end);
+    hp.last_kernel_ms = kernel_ms;
+    hp.last_total_ms = total;
+    hp.last_h2d = h2d;
+    hp.last_d2h = d2h;
+    return BWM_OK;
+}
+
+int bwm_last_host_stats(const bwm_plan* plan, double* kernel_ms, double* total_ms, int64_t* h2d_bytes,
+                        int64_t* d2h_bytes) {
+    if (!plan) return set_err(BWM_E_NULL, "plan is NULL");
+    if (kernel_ms) *kernel_ms = plan->pipe.last_kernel_ms;
+    if (total_ms) *total_ms = plan->pipe.last_total_ms;
+    if (h2d_bytes) *h2d_bytes = plan->pipe.last_h2d;
+    if (d2h_bytes) *d2h_bytes = plan->pipe.last_d2h;
+    return BWM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,115 @@
+// bwm_common.cuh — shared definitions of the BFAST-monitor kernels (sm_100a).
+//
+// Numerics: plain float32 accumulation of beta fails rtol 1e-4 on the
+// MOSUM magnitude.  Three cheap changes fix it (emulated error <= 6e-6 relative):
+//   * y is centred on the pixel's first finite value c (the intercept absorbs it, and the
+//     leading back-fill becomes exactly 0);
+//   * the trend regressor is centred/scaled on the host (M', X': a reparametrisation that
+//     leaves fitted values unchanged in exact arithmetic);
+//   * 16-date FFMA2 block partials are 2Sum-compensated into (hi, lo).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bwm {
+
+constexpr int kThreads = 128;
+constexpr int kTile = 2 * kThreads;   // pixels per CTA tile
+constexpr int kDepth = 16;            // LDG kernel: prefetch depth == compensation block (dates)
+constexpr int kComp = 16;             // dates per 2Sum-compensated block partial
+
+struct KParams {
+    const float* y;             // this launch's pixel 0, row stride ld_y (elements)
+    int64_t ld_y;
+    int64_t n_pixels;
+    int64_t pixel_offset;       // global index of pixel 0 (zero-sigma reporting)
+    int N, n, h, sp;            // sp: padded row stride of the coefficient tables
+    const float* mt;            // [n][sp]  M'^T  (row t = coefficients of date t)
+    const float* xt;            // [N][sp]  X'^T
+    const float* bound;         // [N-n]
+    float inv_dof;              // 1 / (n - p)
+    float sqrt_n;
+    float tc_ts;                // trend_center / trend_scale
+    float inv_ts;               // 1 / trend_scale
+    uint8_t* valid;
+    int32_t* first_idx;
+    float* max_abs;
+    float* beta;
+    float* mo_mean;
+    float* mosum;
+    int64_t ld_out;
+    unsigned long long* zero_sigma;   // atomicMin target (int64 bit pattern, non-negative)
+};
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, f2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 fma2s(float2 a, float s, float2 c) { return __ffma2_rn(a, f2(s, s), c); }
+__device__ __forceinline__ bool finitef(float v) { return fabsf(v) < __int_as_float(0x7f800000); }
+
+// One date of this thread's pixel pair.  Fast path: both pixels exist and the address is
+// 8-byte aligned.  SAFE path (tail tile or odd row stride): scalar, bounds-checked loads.
+template <bool SAFE>
+__device__ __forceinline__ float2 ldp(const float* __restrict__ p, int npx) {
+    if (!SAFE) return __ldg(reinterpret_cast<const float2*>(p));
+    if (npx >= 2) return f2(__ldg(p), __ldg(p + 1));
+    if (npx == 1) return f2(__ldg(p), 0.f);
+    return f2(0.f, 0.f);
+}
+
+// Forward fill in the centred frame: missing -> previous filled value.  `last` starts
+// at 0, i.e. at c, which is exactly the reference's leading back-fill (engine.py:316-317).
+__device__ __forceinline__ float2 fill(float2 v, float2 negc, float2& last) {
+    float2 vc = add2(v, negc);
+    vc.x = finitef(v.x) ? vc.x : last.x;
+    vc.y = finitef(v.y) ? vc.y : last.y;
+    last = vc;
+    return vc;
+}
+
+// hi + lo += b, error-free transformation (Knuth 2Sum).
+__device__ __forceinline__ void two_sum(float2& hi, float2& lo, float2 b) {
+    const float2 s = add2(hi, b);
+    const float2 bb = sub2(s, hi);
+    const float2 e = add2(sub2(hi, sub2(s, bb)), sub2(b, bb));
+    hi = s;
+    lo = add2(lo, e);
+}
+
+// r + sum_i nb_i * x_i   (x: one date's row of the design table in smem)
+template <int NP, int SP>
+__device__ __forceinline__ float2 dot_row(float2 r, const float* __restrict__ xrow, const float2 (&nb)[NP]) {
+    const float4* x4 = reinterpret_cast<const float4*>(xrow);
+#pragma unroll
+    for (int q = 0; q < SP / 4; ++q) {
+        const float4 x = x4[q];
+        if (4 * q + 0 < NP) r = fma2s(nb[4 * q + 0], x.x, r);
+        if (4 * q + 1 < NP) r = fma2s(nb[4 * q + 1], x.y, r);
+        if (4 * q + 2 < NP) r = fma2s(nb[4 * q + 2], x.z, r);
+        if (4 * q + 3 < NP) r = fma2s(nb[4 * q + 3], x.w, r);
+    }
+    return r;
+}
+
+// part_i += vc * m_i
+template <int NP, int SP>
+__device__ __forceinline__ void axpy_row(float2 (&part)[NP], float2 vc, const float* __restrict__ mrow) {
+    const float4* m4 = reinterpret_cast<const float4*>(mrow);
+#pragma unroll
+    for (int q = 0; q < SP / 4; ++q) {
+        const float4 m = m4[q];
+        if (4 * q + 0 < NP) part[4 * q + 0] = fma2s(vc, m.x, part[4 * q + 0]);
+        if (4 * q + 1 < NP) part[4 * q + 1] = fma2s(vc, m.y, part[4 * q + 1]);
+        if (4 * q + 2 < NP) part[4 * q + 2] = fma2s(vc, m.z, part[4 * q + 2]);
+        if (4 * q + 3 < NP) part[4 * q + 3] = fma2s(vc, m.w, part[4 * q + 3]);
+    }
+}
+
+template <int NP>
+struct Coefs {
+    static constexpr int SP = (NP + 3) & ~3;
+};
+
+}  // namespace bwm

@@ -1,0 +1,297 @@
+// bwm_kernel_ldg.cuh — fused BFAST-monitor kernel, register-prefetch variant (sm_100a).
+//
+// Used for the tail tile and for inputs whose rows are not 16-byte aligned (SAFE), and
+// kept as the A/B baseline of the TMA-staged kernel (bwm_kernel_tma.cuh).
+//
+// One CTA = 128 threads = one tile of 256 pixels; one thread owns a pixel PAIR and
+// runs the whole per-pixel pipeline of the reference's fused backend in registers:
+//
+//   reference phase (engine.py)                 here
+//   ---------------------------------------     -------------------------------------------
+//   ingest  _ingest_block  (305-319)            pass 0: first finite value c per pixel
+//                                               fill on the fly: NaN/Inf -> last finite value,
+//                                               leading gap -> c (exact float32 copies)
+//   model   M @ values[:n]  (339-349)           pass 1: beta' = M'(y - c), FFMA2, blocks of
+//                                               16 dates 2Sum-compensated into (hi, lo)
+//   predictions / residuals (351-385)           pass 2: r_t = (y_t - c) - x'_t beta', sigma^2
+//   mosum  _kernels.mosum_block (21-34)         pass 3: window recurrence acc += r_new - r_old
+//   breaks _kernels.detect_block (37-48)                 |MO| max, first strict crossing
+//
+// Memory: the stack is time-major (row t = every pixel at date t), so a warp reading one
+// date of its 64 pixels issues one coalesced 256-byte request (float2 per lane).  Rows are
+// streamed through a 16-deep per-thread register ring; refills run across pass
+// boundaries and into the next tile, so the load pipe never drains between passes.
+// Pass 2 re-reads the history rows pass 1 read moments earlier; they are L2-resident
+// (re-read footprint ~117 KB per resident CTA, ~70 MB chip-wide, L2 = 126 MB), so HBM
+// reads each element of y once.
+//
+// Numerics: see bwm_common.cuh.
+#pragma once
+
+#include "bwm_common.cuh"
+
+namespace bwm {
+
+// RING = true : r_{t-h} comes from a per-thread smem ring of h residuals (h*1 KB per CTA).
+// RING = false: r_{t-h} is recomputed from y_{t-h} by a lagging cursor (an L2 hit: that row
+//               was read h rows earlier) — used when the ring would not fit (large h, C4).
+template <int NP, bool SAFE, bool RING>
+__global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams prm) {
+    constexpr int SP = Coefs<NP>::SP;
+    constexpr int D = kDepth;
+    extern __shared__ __align__(16) float smem[];
+    const int N = prm.N, n = prm.n, h = prm.h;
+    float* s_mt = smem;                       // [n][SP]
+    float* s_xt = s_mt + n * SP;              // [N][SP]
+    float* s_bd = s_xt + N * SP;              // [N-n] (padded to 4)
+    float2* s_ring = reinterpret_cast<float2*>(s_bd + ((N - n + 3) & ~3));   // [h][kThreads]
+
+    // --- constant tables -> smem (once per persistent CTA) -------------------------
+    for (int i = threadIdx.x; i < n * SP; i += kThreads) s_mt[i] = prm.mt[i];
+    for (int i = threadIdx.x; i < N * SP; i += kThreads) s_xt[i] = prm.xt[i];
+    for (int i = threadIdx.x; i < N - n; i += kThreads) s_bd[i] = prm.bound[i];
+    __syncthreads();
+
+    const int tid = threadIdx.x;
+    float2* ring = s_ring + tid;              // this thread's column of the MOSUM ring
+    const int64_t n_tiles = (prm.n_pixels + kTile - 1) / kTile;
+    const int64_t ld = prm.ld_y;
+    const int64_t hld = (int64_t)h * ld;
+    const int wstart = n - h + 1;             // first row of MOSUM window 0 (mosum.py:59)
+
+    int64_t tile = blockIdx.x;
+    if (tile >= n_tiles) return;
+    int64_t px0 = tile * kTile + 2 * tid;
+    int npx = SAFE ? (int)max((int64_t)0, min((int64_t)2, prm.n_pixels - px0)) : 2;
+    const float* yp = prm.y + px0;
+
+    float2 buf[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+        if (k < n) buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);
+
+    for (;;) {
+        const int64_t next_tile = tile + gridDim.x;
+        const bool has_next = next_tile < n_tiles;
+        const int64_t npx0 = has_next ? next_tile * kTile + 2 * tid : px0;
+        const int nnpx = SAFE ? (has_next ? (int)max((int64_t)0, min((int64_t)2, prm.n_pixels - npx0)) : 0) : 2;
+        const float* ynp = prm.y + npx0;
+
+        // ---- pass 0: first finite value per pixel (warp-cooperative early exit) -----
+        float2 c = f2(0.f, 0.f);
+        bool f0 = npx < 1, f1 = npx < 2;
+        for (int t = 0; t < N; t += 4) {
+            if (__all_sync(0xffffffffu, f0 && f1)) break;
+            float2 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                v[k] = (t + k < N) ? ldp<SAFE>(yp + (int64_t)(t + k) * ld, npx)
+                                   : f2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!f0 && finitef(v[k].x)) { c.x = v[k].x; f0 = true; }
+                if (!f1 && finitef(v[k].y)) { c.y = v[k].y; f1 = true; }
+            }
+        }
+        const bool valid0 = (npx >= 1) && f0;
+        const bool valid1 = (npx >= 2) && f1;
+        const float2 negc = f2(-c.x, -c.y);
+
+        // ---- pass 1: beta' = M' (y - c), 2Sum-compensated 16-date blocks ------------
+        float2 hi[NP], lo[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) { hi[i] = f2(0.f, 0.f); lo[i] = f2(0.f, 0.f); }
+        float2 last = f2(0.f, 0.f);
+        const float* pf = yp + (int64_t)D * ld;   // refill target of the row being consumed
+        for (int t0 = 0; t0 < n; t0 += D) {
+            float2 part[NP];
+#pragma unroll
+            for (int i = 0; i < NP; ++i) part[i] = f2(0.f, 0.f);
+            if (t0 + 2 * D <= n) {
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const float2 v = buf[k];
+                    buf[k] = ldp<SAFE>(pf, npx);
+                    pf += ld;
+                    axpy_row<NP, SP>(part, fill(v, negc, last), s_mt + (t0 + k) * SP);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const int t = t0 + k;
+                    if (t < n) {
+                        const float2 v = buf[k];
+                        if (t + D < n) buf[k] = ldp<SAFE>(pf, npx);        // next pass-1 row
+                        else if (k < N) buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);  // pass-2 row k
+                        pf += ld;
+                        axpy_row<NP, SP>(part, fill(v, negc, last), s_mt + t * SP);
+                    } else if (k < N) {
+                        buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);      // free slot: pass-2 row k
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NP; ++i) two_sum(hi[i], lo[i], part[i]);
+        }
+        float2 nb[NP];    // -beta'
+#pragma unroll
+        for (int i = 0; i < NP; ++i) { const float2 b = add2(hi[i], lo[i]); nb[i] = f2(-b.x, -b.y); }
+
+        // ---- pass 2: history residuals, sigma^2, MOSUM window 0 ----------------------
+        float2 ss = f2(0.f, 0.f), acc = f2(0.f, 0.f);
+        last = f2(0.f, 0.f);
+        float2 lag_last = f2(0.f, 0.f);          // !RING: fill state of the lagging cursor
+        float2 lbuf[RING ? 1 : D];               // !RING: prefetched rows t+D-h
+        int slot = wstart % h;                   // ring slot of row t is t mod h
+        pf = yp + (int64_t)D * ld;
+        for (int t0 = 0; t0 < n; t0 += D) {
+            if (t0 + D < wstart && t0 + 2 * D <= N) {
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const float2 v = buf[k];
+                    buf[k] = ldp<SAFE>(pf, npx);
+                    pf += ld;
+                    const float2 r = dot_row<NP, SP>(fill(v, negc, last), s_xt + (t0 + k) * SP, nb);
+                    ss = fma2(r, r, ss);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const int t = t0 + k;
+                    if (t < n) {
+                        const float2 v = buf[k];
+                        if (t + D < N) buf[k] = ldp<SAFE>(pf, npx);
+                        else if (has_next && k < n) buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);
+                        if (!RING && t + D > n && t + D < N) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
+                        pf += ld;
+                        const float2 r = dot_row<NP, SP>(fill(v, negc, last), s_xt + t * SP, nb);
+                        ss = fma2(r, r, ss);
+                        if (t >= wstart) {
+                            acc = add2(acc, r);
+                            if (RING) {
+                                ring[slot * kThreads] = r;
+                                slot = (slot + 1 == h) ? 0 : slot + 1;
+                            }
+                        }
+                        if (!RING && t == wstart - 1) lag_last = last;
+                    }
+                }
+            }
+        }
+        // slot == n mod h now: the slot of r_{n-h}, which window 0 does not contain
+        if (RING) ring[slot * kThreads] = f2(0.f, 0.f);
+
+        // sigma (engine.py:363-371) and the zero-sigma contract (engine.py:373-378)
+        const bool z0 = valid0 && ss.x == 0.f, z1 = valid1 && ss.y == 0.f;
+        if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
+        const float2 var = mul2(ss, f2(prm.inv_dof, prm.inv_dof));
+        float2 inv;
+        inv.x = (valid0 && ss.x > 0.f) ? 1.0f / (sqrtf(var.x) * prm.sqrt_n) : 0.f;
+        inv.y = (valid1 && ss.y > 0.f) ? 1.0f / (sqrtf(var.y) * prm.sqrt_n) : 0.f;
+
+        // switch to the scaled frame: below, residuals and sums are in units of MO
+        if (RING)
+            for (int s = 0; s < h; ++s) ring[s * kThreads] = mul2(ring[s * kThreads], inv);
+        acc = mul2(acc, inv);
+        float2 nbs[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) nbs[i] = mul2(nb[i], inv);
+
+        // ---- pass 3: monitoring period, fused MOSUM + detect -------------------------
+        float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f);
+        int first0 = 0x7fffffff, first1 = 0x7fffffff;
+        float* const mo_out = prm.mosum;
+        // one monitoring row; fast: no bounds checks, refill is the same pass's row t+D
+        auto mon_row = [&](const int k, const int t, const bool fast) {
+            const float2 v = buf[k];
+            if (fast || t + D < N) buf[k] = ldp<SAFE>(pf, npx);
+            else if (has_next && k < n) buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);
+            float2 old = f2(0.f, 0.f);
+            const float2 r = dot_row<NP, SP>(mul2(fill(v, negc, last), inv), s_xt + t * SP, nbs);
+            if (RING) {
+                old = ring[slot * kThreads];
+                ring[slot * kThreads] = r;
+                slot = (slot + 1 == h) ? 0 : slot + 1;
+            } else {
+                if (fast || t > n) {     // r_{t-h}; at t == n, r_{n-h} is outside window 0
+                    const float2 lv = (fast || t >= D) ? lbuf[RING ? 0 : k]
+                                                       : ldp<SAFE>(pf - (int64_t)D * ld - hld, npx);
+                    old = dot_row<NP, SP>(mul2(fill(lv, negc, lag_last), inv), s_xt + (t - h) * SP, nbs);
+                }
+                if (fast || t + D < N) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
+            }
+            pf += ld;
+            acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
+            const int j = t - n;
+            const float b = s_bd[j];
+            const float a0 = fabsf(acc.x), a1 = fabsf(acc.y);
+            mx.x = fmaxf(mx.x, a0);
+            mx.y = fmaxf(mx.y, a1);
+            if (a0 > b) first0 = min(first0, j + 1);  // strict crossing (_kernels.py:47)
+            if (a1 > b) first1 = min(first1, j + 1);
+            msum = add2(msum, acc);
+            if (mo_out) {
+                float* o = mo_out + (int64_t)j * prm.ld_out + px0;
+                if (npx >= 1) o[0] = acc.x;
+                if (npx >= 2) o[1] = acc.y;
+            }
+        };
+        for (int t0 = (n / D) * D; t0 < N; t0 += D) {
+            if (t0 > n && t0 + 2 * D <= N) {
+#pragma unroll
+                for (int k = 0; k < D; ++k) mon_row(k, t0 + k, true);
+            } else {
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const int t = t0 + k;
+                    if (t >= n && t < N) mon_row(k, t, false);
+                    else if (t >= N && has_next && k < n)
+                        buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);   // free slot: next tile
+                }
+            }
+        }
+
+        // ---- outputs --------------------------------------------------------------------
+        if (npx >= 1) {
+            const float inv_m = 1.0f / (float)(N - n);
+            prm.valid[px0] = valid0;
+            prm.first_idx[px0] = first0 == 0x7fffffff ? 0 : first0;
+            prm.max_abs[px0] = mx.x;
+            if (prm.mo_mean) prm.mo_mean[px0] = msum.x * inv_m;
+            if (npx >= 2) {
+                prm.valid[px0 + 1] = valid1;
+                prm.first_idx[px0 + 1] = first1 == 0x7fffffff ? 0 : first1;
+                prm.max_abs[px0 + 1] = mx.y;
+                if (prm.mo_mean) prm.mo_mean[px0 + 1] = msum.y * inv_m;
+            }
+            if (prm.beta) {
+                // back to the raw basis (bwm.h): b0 = c + b0' - b1' tc/ts, b1 = b1'/ts
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (e < npx) {
+                        const bool ok = e == 0 ? valid0 : valid1;
+                        const float ce = e == 0 ? c.x : c.y;
+                        const float b1 = e == 0 ? -nb[1].x : -nb[1].y;
+                        float* o = prm.beta + px0 + e;
+#pragma unroll
+                        for (int i = 0; i < NP; ++i) {
+                            const float bi = e == 0 ? -nb[i].x : -nb[i].y;
+                            float val = bi;
+                            if (i == 0) val = ce + (bi - b1 * prm.tc_ts);
+                            if (i == 1) val = bi * prm.inv_ts;
+                            o[(int64_t)i * prm.ld_out] = ok ? val : 0.f;
+                        }
+                    }
+                }
+            }
+        }
+
+        if (!has_next) break;
+        tile = next_tile;
+        px0 = npx0;
+        npx = nnpx;
+        yp = ynp;
+    }
+}
+
+}  // namespace bwm

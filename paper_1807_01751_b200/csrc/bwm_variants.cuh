@@ -1,0 +1,22 @@
+// bwm_variants.cuh — kernel variant tables (one translation unit per n_params).
+#pragma once
+#include "bwm_kernel_ldg.cuh"
+#include "bwm_kernel_tma.cuh"
+
+namespace bwm {
+enum Kind { kLdgFast = 0, kLdgSafe = 1, kTma = 2 };
+using KernelFn = void (*)(const KParams);
+}  // namespace bwm
+
+// Defines bwm::KernelFn bwm_pick_p<NP>(int kind, bool ring) in the including TU.
+#define BWM_DEFINE_PICK(NP)                                                                      \
+    bwm::KernelFn bwm_pick_p##NP(int kind, bool ring) {                                          \
+        switch (kind) {                                                                          \
+            case bwm::kLdgFast:                                                                  \
+                return ring ? bwm::monitor_kernel_ldg<NP, false, true> : bwm::monitor_kernel_ldg<NP, false, false>; \
+            case bwm::kLdgSafe:                                                                  \
+                return ring ? bwm::monitor_kernel_ldg<NP, true, true> : bwm::monitor_kernel_ldg<NP, true, false>;   \
+            default:                                                                             \
+                return ring ? bwm::monitor_kernel_tma<NP, true> : bwm::monitor_kernel_tma<NP, false>; \
+        }                                                                                        \
+    }

@@ -1,0 +1,4 @@
+// kernels for n_params = 10 (harmonics = 4)
+#include "bwm_variants.cuh"
+
+BWM_DEFINE_PICK(10)

@@ -1,0 +1,4 @@
+// kernels for n_params = 12 (harmonics = 5)
+#include "bwm_variants.cuh"
+
+BWM_DEFINE_PICK(12)

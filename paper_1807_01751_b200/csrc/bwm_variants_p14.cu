@@ -1,0 +1,4 @@
+// kernels for n_params = 14 (harmonics = 6)
+#include "bwm_variants.cuh"
+
+BWM_DEFINE_PICK(14)

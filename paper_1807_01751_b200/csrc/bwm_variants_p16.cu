@@ -1,0 +1,4 @@
+// kernels for n_params = 16 (harmonics = 7)
+#include "bwm_variants.cuh"
+
+BWM_DEFINE_PICK(16)

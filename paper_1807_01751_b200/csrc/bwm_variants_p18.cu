@@ -1,0 +1,4 @@
+// kernels for n_params = 18 (harmonics = 8)
+#include "bwm_variants.cuh"
+
+BWM_DEFINE_PICK(18)

@@ -1,0 +1,4 @@
+// kernels for n_params = 4 (harmonics = 1)
+#include "bwm_variants.cuh"
+
+BWM_DEFINE_PICK(4)

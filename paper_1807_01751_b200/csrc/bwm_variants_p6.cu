@@ -1,0 +1,4 @@
+// kernels for n_params = 6 (harmonics = 2)
+#include "bwm_variants.cuh"
+
+BWM_DEFINE_PICK(6)

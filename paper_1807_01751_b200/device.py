@@ -1,0 +1,193 @@
+"""Device plans: one libbwm plan (constant tables resident on one GPU) per batch geometry.
+
+A plan owns the float32 tables the kernel reads (mapping M', design X', boundary) and is
+reused across calls with the same (axis, freq, k, n, h, lambda, device) — the host f64
+setup runs once, like the reference's per-batch design/mapping (engine.py:339-341).
+
+Two call paths, both through the C ABI (include/bwm.h):
+  run_device : y already in HBM (a torch CUDA tensor)  -> bwm_monitor      (hot call)
+  run_host   : y in host memory (numpy, pinned or not) -> bwm_monitor_host (chunked
+               H2D / kernel / D2H pipeline inside libbwm)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import threading
+import time
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .model import TimeAxis, kernel_basis
+from .mosum import boundary_values
+
+
+@dataclass
+class DeviceResult:
+    """Raw per-pixel maps as produced by the kernel (device tensors or host arrays)."""
+
+    valid: object        # uint8 [P]
+    first_idx: object    # int32 [P]: 0 = none, else 1-based offset into the monitor period
+    max_abs: object      # float32 [P]
+    beta: object = None  # float32 [p, P]
+    mo_mean: object = None   # float32 [P]
+    mosum: object = None     # float32 [N-n, P]
+    zero_sigma: Optional[int] = None   # lowest global pixel with sigma == 0, if any
+    kernel_ms: float = 0.0
+    total_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+
+def _axis_key(axis: TimeAxis) -> str:
+    return hashlib.sha1(np.ascontiguousarray(axis.values).tobytes()).hexdigest()
+
+
+def _as_torch_device(device):
+    import torch
+
+    if device is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device: the bfastmonitor path runs only on the GPU")
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {device!r}")
+    return torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+
+
+class DevicePlan:
+    _cache: dict = {}
+    _lock = threading.Lock()
+
+    def __init__(self, axis: TimeAxis, freq: float, harmonics: int, n_hist: int, bandwidth: int,
+                 crit: float, device=None):
+        lib = _lib.load()
+        self.torch_device = _as_torch_device(device)
+        self.n_obs = len(axis)
+        self.n_hist = int(n_hist)
+        self.bandwidth = int(bandwidth)
+        self.n_params = 2 + 2 * int(harmonics)
+        self.crit = float(crit)
+        basis = kernel_basis(axis, freq, harmonics, n_hist)
+        bound = boundary_values(n_hist, self.n_obs, crit)
+        self._keep = (basis, bound)
+        self.dims = _lib.Dims(self.n_obs, self.n_hist, self.bandwidth, self.n_params)
+        dbl = C.POINTER(C.c_double)
+        tables = _lib.Tables(
+            basis.mapping.ctypes.data_as(dbl),
+            basis.design.ctypes.data_as(dbl),
+            np.ascontiguousarray(bound).ctypes.data_as(dbl),
+            basis.trend_center,
+            basis.trend_scale,
+        )
+        handle = C.c_void_p()
+        _lib.check(lib.bwm_plan_create(C.byref(self.dims), C.byref(tables), self.torch_device.index,
+                                       C.byref(handle)), "bwm_plan_create")
+        self._handle = handle
+        self._lib = lib
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.bwm_plan_destroy(h)
+            except Exception:
+                pass
+
+    @classmethod
+    def get(cls, axis: TimeAxis, freq: float, harmonics: int, n_hist: int, bandwidth: int,
+            crit: float, device=None) -> "DevicePlan":
+        dev = _as_torch_device(device)
+        key = (_axis_key(axis), float(freq), int(harmonics), int(n_hist), int(bandwidth), float(crit), dev.index)
+        with cls._lock:
+            plan = cls._cache.get(key)
+            if plan is None:
+                plan = cls(axis, freq, harmonics, n_hist, bandwidth, crit, dev)
+                if len(cls._cache) > 16:
+                    cls._cache.clear()
+                cls._cache[key] = plan
+            return plan
+
+    # ------------------------------------------------------------------ device path
+    def run_device(self, y, *, keep_mosum: bool = False, beta: bool = False, mean: bool = False,
+                   pixel_offset: int = 0, stream=None, out: Optional[DeviceResult] = None,
+                   check_zero: bool = True) -> DeviceResult:
+        """Monitor a device-resident stack y: float32 CUDA tensor (N, P), unit pixel stride."""
+        import torch
+
+        if not (isinstance(y, torch.Tensor) and y.is_cuda and y.dtype == torch.float32):
+            raise TypeError("run_device needs a float32 CUDA tensor")
+        if y.dim() != 2 or y.shape[0] != self.n_obs:
+            raise ValueError(f"expected y of shape ({self.n_obs}, P), got {tuple(y.shape)}")
+        if y.stride(1) != 1:
+            y = y.contiguous()
+        if y.device != self.torch_device:
+            raise ValueError(f"stack lives on {y.device}, plan on {self.torch_device}")
+        P = int(y.shape[1])
+        dev = self.torch_device
+        if out is None:
+            out = DeviceResult(
+                valid=torch.empty(P, dtype=torch.uint8, device=dev),
+                first_idx=torch.empty(P, dtype=torch.int32, device=dev),
+                max_abs=torch.empty(P, dtype=torch.float32, device=dev),
+                beta=torch.empty((self.n_params, P), dtype=torch.float32, device=dev) if beta else None,
+                mo_mean=torch.empty(P, dtype=torch.float32, device=dev) if mean else None,
+                mosum=torch.empty((self.n_obs - self.n_hist, P), dtype=torch.float32, device=dev)
+                if keep_mosum else None,
+            )
+        zero = torch.full((1,), _lib.INT64_MAX, dtype=torch.int64, device=dev)
+        o = _lib.Outputs(
+            out.valid.data_ptr(), out.first_idx.data_ptr(), out.max_abs.data_ptr(),
+            out.beta.data_ptr() if out.beta is not None else None,
+            out.mo_mean.data_ptr() if out.mo_mean is not None else None,
+            out.mosum.data_ptr() if out.mosum is not None else None,
+            P, zero.data_ptr(),
+        )
+        with torch.cuda.device(dev):
+            s = stream if stream is not None else torch.cuda.current_stream(dev)
+            _lib.check(self._lib.bwm_monitor(self._handle, y.data_ptr(), y.stride(0), P, int(pixel_offset),
+                                             C.byref(o), C.c_void_p(s.cuda_stream)), "bwm_monitor")
+        out.zero_sigma = None
+        out._zero_tensor = zero
+        if check_zero:
+            z = int(zero.item())
+            out.zero_sigma = z if z != _lib.INT64_MAX else None
+        return out
+
+    # ------------------------------------------------------------------ host path
+    def run_host(self, y: np.ndarray, *, keep_mosum: bool = False, beta: bool = False, mean: bool = False,
+                 pixel_offset: int = 0) -> DeviceResult:
+        """Monitor a host stack y: float32 (N, P) C-order numpy array (pinned is fastest)."""
+        y = np.asarray(y)
+        if y.dtype != np.float32 or y.ndim != 2 or y.strides[1] != 4:
+            raise ValueError("run_host needs a float32 (N, P) array with unit pixel stride")
+        if y.shape[0] != self.n_obs:
+            raise ValueError(f"expected y of shape ({self.n_obs}, P), got {y.shape}")
+        P = int(y.shape[1])
+        out = DeviceResult(
+            valid=np.empty(P, dtype=np.uint8),
+            first_idx=np.empty(P, dtype=np.int32),
+            max_abs=np.empty(P, dtype=np.float32),
+            beta=np.empty((self.n_params, P), dtype=np.float32) if beta else None,
+            mo_mean=np.empty(P, dtype=np.float32) if mean else None,
+            mosum=np.empty((self.n_obs - self.n_hist, P), dtype=np.float32) if keep_mosum else None,
+        )
+        zero = np.array([_lib.INT64_MAX], dtype=np.int64)
+        ptr = lambda a: a.ctypes.data if a is not None else None  # noqa: E731
+        o = _lib.Outputs(ptr(out.valid), ptr(out.first_idx), ptr(out.max_abs), ptr(out.beta),
+                         ptr(out.mo_mean), ptr(out.mosum), P, zero.ctypes.data)
+        t0 = time.perf_counter()
+        _lib.check(self._lib.bwm_monitor_host(self._handle, y.ctypes.data, y.strides[0] // 4, P,
+                                              int(pixel_offset), C.byref(o)), "bwm_monitor_host")
+        out.total_ms = (time.perf_counter() - t0) * 1e3
+        k_ms, tot, h2d, d2h = C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
+        self._lib.bwm_last_host_stats(self._handle, C.byref(k_ms), C.byref(tot), C.byref(h2d), C.byref(d2h))
+        out.kernel_ms, out.h2d_bytes, out.d2h_bytes = k_ms.value, h2d.value, d2h.value
+        z = int(zero[0])
+        out.zero_sigma = z if z != _lib.INT64_MAX else None
+        return out

@@ -1,0 +1,128 @@
+"""Synthetic NDVI-like stacks for tests and benchmarks.
+
+  y = 0.5 + 0.2 sin(2 pi t / f + phi_px) + 1e-5 t + eps,   eps ~ N(0, 0.03^2)
+  half the pixels get a level drop c ~ U(-0.3, -0.1) from a random monitoring date on,
+  missing samples: i.i.d. Bernoulli(nan_frac), or clustered "cloud" discs per date,
+  plus a small fraction of dead (all-NaN) pixels.
+
+Two generators with the same recipe: ``host_stack`` (numpy, seeded PCG64; used by the
+tests so a fixture can be regenerated bit-for-bit) and ``device_stack`` (torch on the GPU,
+seeded Philox; used by bench.py for multi-GB stacks).  They are statistically equal, not
+bitwise equal.  Irregular axes follow §8(d): days since the first acquisition, i.i.d.
+U(lo, hi) gaps.  The reference's own generator (synth.py:65-105) is not NDVI-like (mean 0).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Workload:
+    """One BASELINE.json configuration."""
+
+    name: str
+    rows: int            # image rows
+    cols: int            # image cols  -> n_pixels = rows * cols
+    n_obs: int
+    n_hist: int
+    harmonics: int
+    bandwidth: int
+    freq: float
+    nan_frac: float
+    axis: str = "regular"      # "regular" | "irregular"
+    gap: tuple = (1.0, 9.0)    # irregular spacing U(lo, hi) days
+    clustered: bool = False
+    crit: Optional[float] = None
+
+    @property
+    def n_pixels(self) -> int:
+        return self.rows * self.cols
+
+
+# BASELINE.json "configs" (SURVEY.md §8 shorthand C1..C5).  lambda for C1-C3 is the
+# reference's resolve_crit_value at (n=114, h=28, k=3, f=23) measured in SURVEY §8(d).
+WORKLOADS = {
+    "C1": Workload("C1", 128, 128, 228, 114, 3, 28, 23.0, 0.20, crit=2.96519227),
+    "C2": Workload("C2", 4096, 4096, 228, 114, 3, 28, 23.0, 0.20, crit=2.96519227),
+    "C3": Workload("C3", 16384, 16384, 228, 114, 3, 28, 23.0, 0.20, crit=2.96519227),
+    "C4": Workload("C4", 2048, 2048, 1000, 500, 6, 250, 365.25, 0.50, axis="irregular", gap=(1.0, 9.0), crit=3.0),
+    "C5": Workload("C5", 7000, 7000, 400, 200, 3, 50, 365.25, 0.19, axis="irregular", gap=(8.0, 24.0),
+                   clustered=True, crit=3.0),
+}
+
+
+def time_axis(w: Workload, seed: int = 20261017) -> np.ndarray:
+    if w.axis == "regular":
+        return np.arange(1.0, w.n_obs + 1.0)
+    rng = np.random.default_rng(seed)
+    gaps = rng.uniform(w.gap[0], w.gap[1], w.n_obs - 1)
+    return np.concatenate([[1.0], 1.0 + np.cumsum(gaps)])
+
+
+def host_stack(n_pixels: int, t: np.ndarray, freq: float, n_hist: int, nan_frac: float, seed: int,
+               clustered: bool = False, dead_frac: float = 1e-4, cols: Optional[int] = None) -> np.ndarray:
+    """float32 (N, P) NDVI-like stack on the host (numpy)."""
+    rng = np.random.default_rng(seed)
+    N = t.size
+    phi = rng.uniform(0.0, 2.0 * np.pi, n_pixels)
+    y = 0.5 + 0.2 * np.sin(2.0 * np.pi * t[:, None] / freq + phi[None, :]) + 1e-5 * t[:, None]
+    y += rng.normal(0.0, 0.03, (N, n_pixels))
+    brk = rng.random(n_pixels) < 0.5
+    start = rng.integers(n_hist, N, n_pixels)
+    drop = rng.uniform(-0.3, -0.1, n_pixels)
+    y += ((np.arange(N)[:, None] >= start[None, :]) & brk[None, :]) * drop[None, :]
+    y = y.astype(np.float32)
+    if clustered:
+        y[_cloud_mask(rng, N, n_pixels, cols or int(np.sqrt(n_pixels)))] = np.nan
+    else:
+        y[rng.random((N, n_pixels)) < nan_frac] = np.nan
+    dead = rng.random(n_pixels) < dead_frac
+    y[:, dead] = np.nan
+    return y
+
+
+def _cloud_mask(rng, N: int, P: int, cols: int) -> np.ndarray:
+    """Per-date random discs (radius U(20,150) px, 0-5 per 512^2 area), §8(d) C5."""
+    rows = (P + cols - 1) // cols
+    mask = np.zeros((N, P), dtype=bool)
+    rr, cc = np.divmod(np.arange(P), cols)
+    per = max(1.0, rows * cols / 512.0**2)
+    for d in range(N):
+        for _ in range(rng.integers(0, int(round(5 * per)) + 1)):
+            r0, c0 = rng.uniform(0, rows), rng.uniform(0, cols)
+            rad = rng.uniform(20, 150)
+            mask[d] |= (rr - r0) ** 2 + (cc - c0) ** 2 <= rad * rad
+    return mask
+
+
+def device_stack(n_pixels: int, t: np.ndarray, freq: float, n_hist: int, nan_frac: float, seed: int,
+                 device="cuda", out=None, chunk: int = 1 << 22):
+    """float32 (N, P) NDVI-like stack generated directly in HBM (torch Philox)."""
+    import torch
+
+    N = t.size
+    dev = torch.device(device)
+    if out is None:
+        out = torch.empty((N, n_pixels), dtype=torch.float32, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    tt = torch.as_tensor(t, dtype=torch.float32, device=dev)[:, None]
+    rows = torch.arange(N, device=dev)[:, None]
+    for p0 in range(0, n_pixels, chunk):
+        w = min(chunk, n_pixels - p0)
+        phi = torch.rand(w, generator=g, device=dev) * (2 * np.pi)
+        blk = 0.5 + 0.2 * torch.sin(2 * np.pi * tt / freq + phi[None, :]) + 1e-5 * tt
+        blk += 0.03 * torch.randn((N, w), generator=g, device=dev)
+        brk = torch.rand(w, generator=g, device=dev) < 0.5
+        start = torch.randint(n_hist, N, (w,), generator=g, device=dev)
+        drop = -0.1 - 0.2 * torch.rand(w, generator=g, device=dev)
+        blk += ((rows >= start[None, :]) & brk[None, :]) * drop[None, :]
+        blk[torch.rand((N, w), generator=g, device=dev) < nan_frac] = float("nan")
+        dead = torch.rand(w, generator=g, device=dev) < 1e-4
+        blk[:, dead] = float("nan")
+        out[:, p0:p0 + w] = blk
+    return out

@@ -1,0 +1,224 @@
+"""Parity of the CUDA path (libbwm through the C ABI) against the reference's golden
+outputs and the CPU oracle.  Tolerances (BASELINE.json north_star):
+
+  valid        identical
+  first_break  identical on every pixel that is not borderline (a window j <= the later of
+               the two first crossings with | |MO_ref,j| - b_j | <= 1e-4 b_j)
+  max_abs_mo   rtol 1e-4
+  mosum_mean   |d| <= 1e-4 * max(|mean_ref|, max_abs_ref)  (a mean of signed terms)
+  beta         |d_i| <= 1e-4 |beta_ref,i| + 1e-4 ||M_i,:||_1 ||y_hist||_inf
+"""
+
+import numpy as np
+import pytest
+
+from oracle import bfast_oracle as bo
+from tests.golden_cases import CASES, load
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+
+
+def _pkg():
+    import paper_1807_01751_b200 as pkg
+
+    return pkg
+
+
+def check_parity(case, first_break, max_abs, valid, mean=None, beta=None, mosum=None):
+    n_mon = case.y.shape[0] - case.n
+    P = case.y.shape[1]
+    assert np.array_equal(valid, case.valid), "valid mask differs"
+    first_gpu = np.where(first_break > 0, first_break - case.n, 0)
+    border = bo.borderline_from_pairs(case.near, n_mon, P, case.first_idx, first_gpu)
+    bad = np.flatnonzero((first_gpu != case.first_idx) & ~border)
+    assert bad.size == 0, f"{case.name}: {bad.size} non-borderline break mismatches, e.g. {bad[:5]}"
+    np.testing.assert_allclose(max_abs, case.max_abs_mo, rtol=RTOL, atol=0)
+    if mean is not None:
+        scale = np.maximum(np.abs(case.mosum_mean), case.max_abs_mo)
+        assert np.all(np.abs(mean - case.mosum_mean) <= RTOL * scale + 1e-30)
+    if beta is not None and case.beta is not None:
+        X = bo.design_matrix(case.t, case.freq, case.k)
+        M = bo.mapping_matrix(X, case.n)
+        filled, _ = bo.fill_block(case.y)
+        yinf = np.abs(filled[:case.n]).max(axis=0)
+        tol = RTOL * np.abs(case.beta) + RTOL * np.abs(M).sum(axis=1)[:, None] * yinf[None, :]
+        assert np.all(np.abs(beta - case.beta) <= tol), f"{case.name}: beta out of tolerance"
+    if mosum is not None and case.mosum is not None:
+        scale = np.maximum(case.max_abs_mo, 1e-30)[None, :]
+        assert np.all(np.abs(mosum - case.mosum) <= RTOL * scale)
+    return int(border.sum())
+
+
+def config_for(case, backend="fused"):
+    return _pkg().MonitorConfig(history=case.n, bandwidth=case.h, harmonics=case.k, freq=case.freq,
+                                crit_value=case.crit, backend=backend)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_parity_host_path(name):
+    pkg = _pkg()
+    case = load(name)
+    stack = pkg.SeriesStack(case.y, pkg.TimeAxis(case.t))
+    bm = pkg.monitor_batch(stack, config_for(case), keep_mosum=True, return_beta=True, return_mean=True)
+    assert bm.first_break.dtype == np.int64 and bm.max_abs_mo.dtype == np.float64 and bm.valid.dtype == bool
+    check_parity(case, bm.first_break, bm.max_abs_mo, bm.valid, bm.mosum_mean, bm.beta, bm.mosum)
+    assert np.array_equal(bm.detected, bm.first_break > 0)
+    assert bm.crit_value == case.crit
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_parity_device_path(name):
+    import torch
+
+    pkg = _pkg()
+    case = load(name)
+    y = torch.as_tensor(case.y, device="cuda")
+    stack = pkg.SeriesStack(y, pkg.TimeAxis(case.t))
+    bm = pkg.monitor_batch(stack, config_for(case, "cuda"), keep_mosum=True, return_beta=True, return_mean=True)
+    check_parity(case, bm.first_break, bm.max_abs_mo, bm.valid, bm.mosum_mean, bm.beta, bm.mosum)
+
+
+def _plan(case, env=None, monkeypatch=None):
+    from paper_1807_01751_b200.device import DevicePlan
+    from paper_1807_01751_b200.model import TimeAxis
+
+    if env is not None:
+        monkeypatch.setenv("BWM_KERNEL", env)
+    plan = DevicePlan(TimeAxis(case.t), case.freq, case.k, case.n, case.h, case.crit, "cuda")
+    if env is not None:
+        monkeypatch.delenv("BWM_KERNEL")
+    return plan
+
+
+def _maps(res):
+    return [None if a is None else a.cpu().numpy() for a in (res.valid, res.first_idx, res.max_abs, res.mo_mean, res.beta)]
+
+
+@pytest.mark.parametrize("name", ["c1", "c4_tile", "odd_pixels_k8", "edges_h10_k2", "lag_h100"])
+def test_kernel_variants_bit_identical(name, monkeypatch):
+    """TMA-staged kernel, register-prefetch kernel and the scalar safe kernel (misaligned
+    input) run the same arithmetic in the same order: results must match bit for bit."""
+    import torch
+
+    case = load(name)
+    y = torch.as_tensor(case.y, device="cuda")
+    tma = _maps(_plan(case).run_device(y, beta=True, mean=True))
+    ldg = _maps(_plan(case, "ldg", monkeypatch).run_device(y, beta=True, mean=True))
+    # misaligned view: pixel 0 at a 4-byte offset -> safe kernel for every tile
+    big = torch.empty((y.shape[0], y.shape[1] + 1), device="cuda")
+    big[:, 1:] = y
+    safe = _maps(_plan(case).run_device(big[:, 1:], beta=True, mean=True))
+    for a, b, c in zip(tma, ldg, safe):
+        assert np.array_equal(a, b, equal_nan=True)
+        assert np.array_equal(a, c, equal_nan=True)
+
+
+@pytest.mark.parametrize("shards", [2, 3, 8])
+def test_shard_invariance(shards):
+    """Results are bit-identical whatever the pixel sharding (the GPU analogue of
+    test_engine.py:170-181 'results do not depend on the worker count')."""
+    import torch
+
+    case = load("c1")
+    plan = _plan(case)
+    y = torch.as_tensor(case.y, device="cuda")
+    whole = _maps(plan.run_device(y, mean=True))
+    P = y.shape[1]
+    edges = np.linspace(0, P, shards + 1).astype(int)
+    edges[1:-1] = (edges[1:-1] // 2) * 2          # keep float2 alignment of each shard
+    parts = [_maps(plan.run_device(y[:, a:b], mean=True, pixel_offset=int(a))) for a, b in zip(edges[:-1], edges[1:])]
+    for i in range(4):
+        assert np.array_equal(whole[i], np.concatenate([p[i] for p in parts]))
+
+
+def test_host_and_device_paths_identical():
+    import torch
+
+    case = load("c5_tile")
+    plan = _plan(case)
+    host = plan.run_host(case.y, beta=True, mean=True, keep_mosum=True)
+    dev = plan.run_device(torch.as_tensor(case.y, device="cuda"), beta=True, mean=True, keep_mosum=True)
+    for a, b in [(host.valid, dev.valid), (host.first_idx, dev.first_idx), (host.max_abs, dev.max_abs),
+                 (host.mo_mean, dev.mo_mean), (host.beta, dev.beta), (host.mosum, dev.mosum)]:
+        assert np.array_equal(a, b.cpu().numpy())
+    assert host.h2d_bytes == case.y.nbytes
+
+
+def test_zero_sigma_raises_for_lowest_pixel():
+    import json
+
+    from tests.golden_cases import GOLDEN
+
+    pkg = _pkg()
+    z = np.load(GOLDEN / "zero_sigma.npz")
+    info = json.loads(str(z["info"]))
+    cfg = pkg.MonitorConfig(history=100, bandwidth=50, harmonics=3, freq=23.0, crit_value=4.9)
+    with pytest.raises(pkg.ZeroResidualError, match=info["message"]):
+        pkg.monitor_batch(pkg.SeriesStack(z["y"], pkg.regular_axis(200)), cfg)
+
+
+def test_determinism_and_permutation_equivariance():
+    import torch
+
+    case = load("c4_tile")
+    plan = _plan(case)
+    y = torch.as_tensor(case.y, device="cuda")
+    a = _maps(plan.run_device(y, mean=True))
+    b = _maps(plan.run_device(y, mean=True))
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v, equal_nan=True)
+    perm = torch.randperm(y.shape[1], generator=torch.Generator().manual_seed(3)).cuda()
+    c = _maps(plan.run_device(y[:, perm].contiguous(), mean=True))
+    p = perm.cpu().numpy()
+    for u, v in zip(a[:4], c[:4]):
+        assert np.array_equal(u[p], v)
+
+
+@pytest.mark.parametrize("wname", ["C2", "C4", "C5"])
+def test_large_stack_sampled_tiles(wname):
+    """Full-size kernels on device-generated stacks; sampled tiles checked against the oracle
+    (the f64 oracle of a whole C2 stack would need ~124 GB of host RAM)."""
+    import torch
+
+    from paper_1807_01751_b200.device import DevicePlan
+    from paper_1807_01751_b200.model import TimeAxis
+    from paper_1807_01751_b200.synth import WORKLOADS, device_stack, time_axis
+
+    w = WORKLOADS[wname]
+    t = time_axis(w)
+    P = {"C2": 1 << 21, "C4": 1 << 18, "C5": 1 << 20}[wname]      # bounded for test time
+    y = device_stack(P, t, w.freq, w.n_hist, w.nan_frac, seed=20261017, device="cuda")
+    plan = DevicePlan(TimeAxis(t), w.freq, w.harmonics, w.n_hist, w.bandwidth, w.crit, "cuda")
+    res = plan.run_device(y, mean=True)
+    valid, first, mx, mean, _ = _maps(res)
+    rng = np.random.default_rng(1)
+    tiles = sorted(set(rng.integers(0, P // 256, 3).tolist()) | {P // 256 - 1})
+    for tile in tiles:
+        sl = slice(tile * 256, tile * 256 + 256)
+        ys = y[:, sl].cpu().numpy()
+        r = bo.monitor(ys, t, w.n_hist, w.bandwidth, w.harmonics, w.freq, w.crit, keep_mosum=True)
+        assert np.array_equal(valid[sl].astype(bool), r.valid)
+        border = bo.borderline(r.mosum, r.bound, r.first_idx, first[sl].astype(np.int64))
+        assert not np.any((first[sl] != r.first_idx) & ~border)
+        np.testing.assert_allclose(mx[sl], r.max_abs_mo, rtol=RTOL)
+    # size-independent properties of the whole stack
+    assert np.all((first >= 0) & (first <= t.size - w.n_hist))
+    assert np.all(mx[valid == 0] == 0) and np.all(first[valid == 0] == 0)
+    assert np.all(np.abs(mean) <= mx + 1e-6)
+    del y
+    torch.cuda.empty_cache()
+
+
+def test_critical_value_matches_pinned():
+    """lambda through the GPU kernel vs the reference's pinned value (test_mosum.py:20)."""
+    import json
+
+    from tests.golden_cases import GOLDEN
+
+    pkg = _pkg()
+    pinned = json.loads((GOLDEN / "pinned.json").read_text())["crit_20k"]
+    req = pkg.CriticalValueRequest(**pinned["request"])
+    lam = pkg.critical_value(req, threads=8)
+    assert lam == pytest.approx(pinned["value"], rel=2e-5)
