@@ -17,7 +17,7 @@
 #include <string>
 #include <vector>
 
-#define BWM_DECLARE_PICK(NP) bwm::KernelFn bwm_pick_p##NP(int kind, bool ring);
+#define BWM_DECLARE_PICK(NP) bwm::KernelFn bwm_pick_p##NP(int kind, int mode);
 // per-n_params kernel tables, one translation unit each (bwm_variants_p*.cu)
 BWM_DECLARE_PICK(4)
 BWM_DECLARE_PICK(6)
@@ -63,10 +63,31 @@ int64_t smem_bytes_for(int N, int n, int h, int p, bool ring) {
     return bytes;
 }
 
-// shared memory of the TMA kernel: stage ring + the above + 2*kStages mbarriers
-int64_t smem_bytes_tma(int N, int n, int h, int p, bool ring) {
-    return bwm::kStages * bwm::tma_stage_bytes(ring) + smem_bytes_for(N, n, h, p, ring) +
-           2 * bwm::kStages * 8;
+// TMA kernel ring mode for a bandwidth h (bwm_kernel_tma.cuh): a TMEM ring of L rows (+8
+// mirror rows, 2 columns each) when 8 <= h and it fits 256 columns; a shared-memory ring for
+// h < 8; the lagging cursor above.
+struct TmaRing {
+    int mode, rows, cols;
+};
+TmaRing tma_ring_for(int h) {
+    const int L = ((h + 7) / 8) * 8;
+    const int need = 2 * (L + 8);
+    if (h >= 8 && need <= 256) {
+        int cols = 32;
+        while (cols < need) cols *= 2;
+        return {bwm::kRingTmem, L, cols};
+    }
+    return {h < 8 ? (int)bwm::kRingSmem : (int)bwm::kRingLag, 0, 0};
+}
+
+// shared memory of the TMA kernel: stages + tables (bound indexed by row) + smem ring
+// (kRingSmem only) + 2*kStages mbarriers + the TMEM address slot
+int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
+    const int sp = (p + 3) & ~3;
+    int64_t fl = (int64_t)n * sp + (int64_t)N * sp + ((N + 3) & ~3);
+    int64_t bytes = bwm::kStages * bwm::tma_stage_bytes(mode) + fl * 4;
+    if (mode == bwm::kRingSmem) bytes += (int64_t)h * bwm::kThreads * 8;
+    return bytes + 2 * bwm::kStages * 8 + 16;
 }
 
 using bwm::Kind;
@@ -88,17 +109,17 @@ struct DeviceRestore {
     }
 };
 
-// (n_params, kind, ring) -> kernel.  kLdgSafe: tail tile / misaligned input (scalar loads).
-KernelFn pick(int p, Kind kind, bool ring) {
+// (n_params, kind, mode) -> kernel.  kLdgSafe: tail tile / misaligned input (scalar loads).
+KernelFn pick(int p, Kind kind, int mode) {
     switch (p) {
-        case 4: return bwm_pick_p4(kind, ring);
-        case 6: return bwm_pick_p6(kind, ring);
-        case 8: return bwm_pick_p8(kind, ring);
-        case 10: return bwm_pick_p10(kind, ring);
-        case 12: return bwm_pick_p12(kind, ring);
-        case 14: return bwm_pick_p14(kind, ring);
-        case 16: return bwm_pick_p16(kind, ring);
-        case 18: return bwm_pick_p18(kind, ring);
+        case 4: return bwm_pick_p4(kind, mode);
+        case 6: return bwm_pick_p6(kind, mode);
+        case 8: return bwm_pick_p8(kind, mode);
+        case 10: return bwm_pick_p10(kind, mode);
+        case 12: return bwm_pick_p12(kind, mode);
+        case 14: return bwm_pick_p14(kind, mode);
+        case 16: return bwm_pick_p16(kind, mode);
+        case 18: return bwm_pick_p18(kind, mode);
         default: return nullptr;
     }
 }
@@ -134,7 +155,8 @@ struct bwm_plan {
     float* d_xt = nullptr;
     float* d_bound = nullptr;
     float inv_dof = 0, sqrt_n = 0, tc_ts = 0, inv_ts = 0;
-    bool ring = true;
+    bool ring = true;                  // LDG kernels: smem ring (else lagging cursor)
+    TmaRing tring{};                   // TMA kernel ring mode
     int64_t smem = 0;                  // LDG kernels
     int64_t smem_tma = 0;              // TMA kernel (0: does not fit -> LDG kernels only)
     int sms = 0;
@@ -170,7 +192,8 @@ int64_t bwm_smem_bytes(const bwm_dims* d) {
     int rc = validate_dims(d);
     if (rc) return rc;
     const bool ring = d->bandwidth <= kRingMaxH;
-    return smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, ring);
+    (void)ring;
+    return smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, tma_ring_for(d->bandwidth).mode);
 }
 
 int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_plan** out_plan) {
@@ -194,7 +217,8 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     plan->sp = sp;
     plan->ring = h <= kRingMaxH;
     plan->smem = smem_bytes_for(N, n, h, p, plan->ring);
-    plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->ring);
+    plan->tring = tma_ring_for(h);
+    plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->tring.mode);
     const char* env = getenv("BWM_KERNEL");
     plan->force_ldg = env && strcmp(env, "ldg") == 0;
     plan->inv_dof = (float)(1.0 / (double)(n - p));
@@ -244,7 +268,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         const Kind kind = (Kind)v;
         const int64_t sm = kind == kTma ? plan->smem_tma : plan->smem;
         if (kind == kTma && sm == 0) continue;
-        KernelFn fn = pick(p, kind, plan->ring);
+        KernelFn fn = pick(p, kind, kind == kTma ? plan->tring.mode : (plan->ring ? 0 : (int)bwm::kRingLag));
         if ((e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sm)) != cudaSuccess)
             return fail(e, "cudaFuncSetAttribute");
@@ -252,6 +276,8 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, threads_of(kind),
                                                                (size_t)sm)) != cudaSuccess)
             return fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+        if (kind == kTma && plan->tring.mode == bwm::kRingTmem)
+            nb = std::min(nb, 512 / plan->tring.cols);   // TMEM columns per SM
         plan->blocks_per_sm[v] = std::max(nb, 1);
     }
     *out_plan = plan;
@@ -323,6 +349,8 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     k.bound = plan->d_bound;
     k.inv_dof = plan->inv_dof;
     k.sqrt_n = plan->sqrt_n;
+    k.ring_rows = plan->tring.rows;
+    k.tmem_cols = plan->tring.cols;
     k.tc_ts = plan->tc_ts;
     k.inv_ts = plan->inv_ts;
     k.valid = out->valid;
@@ -363,7 +391,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         kp.beta = out->beta ? out->beta + p0 : nullptr;
         kp.mo_mean = out->mo_mean ? out->mo_mean + p0 : nullptr;
         kp.mosum = out->mosum ? out->mosum + p0 : nullptr;
-        KernelFn fn = pick(d.n_params, kind, plan->ring);
+        KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode : (plan->ring ? 0 : (int)bwm::kRingLag));
         const int64_t tiles = (cnt + bwm::kTile - 1) / bwm::kTile;
         const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * plan->blocks_per_sm[kind]);
         const size_t sm = (size_t)(kind == kTma ? plan->smem_tma : plan->smem);

@@ -29,6 +29,8 @@ struct KParams {
     const float* bound;         // [N-n]
     float inv_dof;              // 1 / (n - p)
     float sqrt_n;
+    int ring_rows;              // TMEM ring: L (multiple of 8, >= h); rows L..L+7 mirror 0..7
+    int tmem_cols;              // TMEM columns allocated per CTA (power of 2 >= 32)
     float tc_ts;                // trend_center / trend_scale
     float inv_ts;               // 1 / trend_scale
     uint8_t* valid;
@@ -105,6 +107,18 @@ __device__ __forceinline__ void axpy_row(float2 (&part)[NP], float2 vc, const fl
         if (4 * q + 2 < NP) part[4 * q + 2] = fma2s(vc, m.z, part[4 * q + 2]);
         if (4 * q + 3 < NP) part[4 * q + 3] = fma2s(vc, m.w, part[4 * q + 3]);
     }
+}
+
+// Finish a pixel pair after the monitoring pass, in the unscaled frame: the kernel tracks
+// max |acc| and the window-sum total; MO = acc / (sigma sqrt n).  sigma == 0 (constant
+// history) gives inv = 2^100: every non-zero window then crossed (b * 0 = 0), matching the
+// reference's round-off-sigma behaviour, and the reported magnitude is huge.
+__device__ __forceinline__ float2 sigma_scale(float2 ss, float inv_dof, float sqrt_n, bool v0, bool v1) {
+    const float2 var = mul2(ss, f2(inv_dof, inv_dof));
+    return f2(v0 ? sqrtf(var.x) * sqrt_n : 0.f, v1 ? sqrtf(var.y) * sqrt_n : 0.f);
+}
+__device__ __forceinline__ float2 inv_scale(float2 s) {
+    return f2(s.x > 0.f ? 1.0f / s.x : 0x1p100f, s.y > 0.f ? 1.0f / s.y : 0x1p100f);
 }
 
 template <int NP>

@@ -181,21 +181,11 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         // slot == n mod h now: the slot of r_{n-h}, which window 0 does not contain
         if (RING) ring[slot * kThreads] = f2(0.f, 0.f);
 
-        // sigma (engine.py:363-371) and the zero-sigma contract (engine.py:373-378)
-        const bool z0 = valid0 && ss.x == 0.f, z1 = valid1 && ss.y == 0.f;
+        // sigma and the zero-sigma contract: see bwm_kernel_tma.cuh (identical arithmetic)
+        const bool z0 = valid0 && ss.x == 0.f && c.x == 0.f, z1 = valid1 && ss.y == 0.f && c.y == 0.f;
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
-        const float2 var = mul2(ss, f2(prm.inv_dof, prm.inv_dof));
-        float2 inv;
-        inv.x = (valid0 && ss.x > 0.f) ? 1.0f / (sqrtf(var.x) * prm.sqrt_n) : 0.f;
-        inv.y = (valid1 && ss.y > 0.f) ? 1.0f / (sqrtf(var.y) * prm.sqrt_n) : 0.f;
-
-        // switch to the scaled frame: below, residuals and sums are in units of MO
-        if (RING)
-            for (int s = 0; s < h; ++s) ring[s * kThreads] = mul2(ring[s * kThreads], inv);
-        acc = mul2(acc, inv);
-        float2 nbs[NP];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) nbs[i] = mul2(nb[i], inv);
+        const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);
+        const float2 inv = inv_scale(sc);
 
         // ---- pass 3: monitoring period, fused MOSUM + detect -------------------------
         float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f);
@@ -207,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
             if (fast || t + D < N) buf[k] = ldp<SAFE>(pf, npx);
             else if (has_next && k < n) buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);
             float2 old = f2(0.f, 0.f);
-            const float2 r = dot_row<NP, SP>(mul2(fill(v, negc, last), inv), s_xt + t * SP, nbs);
+            const float2 r = dot_row<NP, SP>(fill(v, negc, last), s_xt + t * SP, nb);
             if (RING) {
                 old = ring[slot * kThreads];
                 ring[slot * kThreads] = r;
@@ -216,24 +206,26 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                 if (fast || t > n) {     // r_{t-h}; at t == n, r_{n-h} is outside window 0
                     const float2 lv = (fast || t >= D) ? lbuf[RING ? 0 : k]
                                                        : ldp<SAFE>(pf - (int64_t)D * ld - hld, npx);
-                    old = dot_row<NP, SP>(mul2(fill(lv, negc, lag_last), inv), s_xt + (t - h) * SP, nbs);
+                    old = dot_row<NP, SP>(fill(lv, negc, lag_last), s_xt + (t - h) * SP, nb);
                 }
                 if (fast || t + D < N) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
             }
             pf += ld;
             acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
             const int j = t - n;
-            const float b = s_bd[j];
+            const float bj = s_bd[j];
+            const float2 bs = mul2(sc, f2(bj, bj));    // boundary in the unscaled frame
             const float a0 = fabsf(acc.x), a1 = fabsf(acc.y);
             mx.x = fmaxf(mx.x, a0);
             mx.y = fmaxf(mx.y, a1);
-            if (a0 > b) first0 = min(first0, j + 1);  // strict crossing (_kernels.py:47)
-            if (a1 > b) first1 = min(first1, j + 1);
+            if (a0 > bs.x) first0 = min(first0, j + 1);  // strict crossing (_kernels.py:47)
+            if (a1 > bs.y) first1 = min(first1, j + 1);
             msum = add2(msum, acc);
             if (mo_out) {
+                const float2 mo = mul2(acc, inv);
                 float* o = mo_out + (int64_t)j * prm.ld_out + px0;
-                if (npx >= 1) o[0] = acc.x;
-                if (npx >= 2) o[1] = acc.y;
+                if (npx >= 1) o[0] = mo.x;
+                if (npx >= 2) o[1] = mo.y;
             }
         };
         for (int t0 = (n / D) * D; t0 < N; t0 += D) {
@@ -256,13 +248,14 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
             const float inv_m = 1.0f / (float)(N - n);
             prm.valid[px0] = valid0;
             prm.first_idx[px0] = first0 == 0x7fffffff ? 0 : first0;
-            prm.max_abs[px0] = mx.x;
-            if (prm.mo_mean) prm.mo_mean[px0] = msum.x * inv_m;
+            const float2 mxs = mul2(mx, inv), mean = mul2(mul2(msum, inv), f2(inv_m, inv_m));
+            prm.max_abs[px0] = mxs.x;
+            if (prm.mo_mean) prm.mo_mean[px0] = mean.x;
             if (npx >= 2) {
                 prm.valid[px0 + 1] = valid1;
                 prm.first_idx[px0 + 1] = first1 == 0x7fffffff ? 0 : first1;
-                prm.max_abs[px0 + 1] = mx.y;
-                if (prm.mo_mean) prm.mo_mean[px0 + 1] = msum.y * inv_m;
+                prm.max_abs[px0 + 1] = mxs.y;
+                if (prm.mo_mean) prm.mo_mean[px0 + 1] = mean.y;
             }
             if (prm.beta) {
                 // back to the raw basis (bwm.h): b0 = c + b0' - b1' tc/ts, b1 = b1'/ts

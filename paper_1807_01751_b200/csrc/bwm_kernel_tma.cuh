@@ -5,16 +5,27 @@
 // one date) from HBM/L2 into a ring of shared-memory stages with bulk asynchronous copies
 // (cp.async.bulk -> the TMA engine, SASS UBLKCP), signalling an mbarrier per stage with
 // complete_tx; consumers wait on the stage, read their float2 per row (LDS.64,
-// conflict-free) and release the stage with one arrive per warp.  Registers therefore
-// hold only the per-pixel pipeline state, and the number of bytes in flight per SM is set
-// by the stage ring (kStages x kStageRows KB per CTA), not by register pressure.
+// conflict-free) and release the stage with one arrive per warp.  Registers hold only the
+// per-pixel pipeline state; bytes in flight per SM are set by the stage ring.
 //
 // Row stream per tile (the producer runs ahead across passes and tiles):
-//   pass 1 : rows [0, n)      beta' = M'(y - c)        (pass 0 scans the first stage for c)
-//   pass 2 : rows [0, n)      residuals, sigma^2, MOSUM window 0   (re-read: L2 hit)
-//   pass 3 : rows [n, N)      MOSUM recurrence + detect; with !RING each stage also carries
-//                             rows t-h (the lagging cursor's input, L2 hit)
-// Reference phases: see bwm_common.cuh / bwm_kernel_ldg.cuh (same arithmetic).
+//   pass 1 : rows [0, n)             beta' = M'(y - c)     (pass 0 scans the first stage for c)
+//   pass 2 : rows [0, n)             residuals, sigma^2, MOSUM window 0   (re-read: L2 hit)
+//   pass 3 : rows [8*floor(n/8), N)  MOSUM recurrence + detect (stages 8-row aligned);
+//            LAG mode: each stage also carries rows t-h (the lagging cursor's input)
+//
+// MOSUM residual ring (r_{t-h} for the add-one/drop-one recurrence, _kernels.py:31-34):
+//   MODE kRingTmem : in Tensor Memory.  Each thread owns its TMEM lane; ring row q of the
+//                    pixel pair occupies columns 2q, 2q+1.  L = ring rows (multiple of 8,
+//                    >= h) plus 8 mirror rows (L+k == k) so an 8-row window read
+//                    starting anywhere in [0, L) never wraps: one tcgen05.ld.x16 and one
+//                    tcgen05.st.x16 per stage instead of 8 shared loads/stores + index math.
+//   MODE kRingSmem : per-thread shared-memory ring of h rows (small h < 8).
+//   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged row t-h (large h).
+//
+// The monitoring pass runs in the UNSCALED frame: acc = sum of window residuals, crossing
+// test |acc| > b_j * sigma * sqrt(n) (== |MO_j| > b_j), MO = acc / (sigma sqrt n) applied to
+// the max/mean at the end.
 #pragma once
 
 #include "bwm_common.cuh"
@@ -22,10 +33,12 @@
 namespace bwm {
 
 constexpr int kStageRows = 8;                   // dates per stage
-constexpr int kStages = 4;                      // stage ring depth
+constexpr int kStages = 7;                      // stage ring depth
 constexpr int kRowBytes = kTile * 4;            // one date of one tile
 constexpr int kConsumerWarps = kThreads / 32;
 constexpr int kTmaThreads = kThreads + 32;      // + producer warp
+
+enum RingMode { kRingSmem = 0, kRingTmem = 1, kRingLag = 2 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -57,33 +70,81 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-// Shared-memory footprint of the TMA kernel (host mirror in bwm_capi.cu).
-__host__ __device__ constexpr int64_t tma_stage_bytes(bool ring) {
-    return (int64_t)kStageRows * kRowBytes * (ring ? 1 : 2);
+// ---- Tensor Memory (tcgen05) helpers: the per-thread residual ring -------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t cols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 16 consecutive 32-bit columns of this thread's lane (8 ring rows of the pixel pair)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float2 (&v)[8]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+    tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = f2(__uint_as_float(r[2 * k]), __uint_as_float(r[2 * k + 1]));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float2 (&v)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(__float_as_uint(v[0].x)), "r"(__float_as_uint(v[0].y)), "r"(__float_as_uint(v[1].x)),
+        "r"(__float_as_uint(v[1].y)), "r"(__float_as_uint(v[2].x)), "r"(__float_as_uint(v[2].y)),
+        "r"(__float_as_uint(v[3].x)), "r"(__float_as_uint(v[3].y)), "r"(__float_as_uint(v[4].x)),
+        "r"(__float_as_uint(v[4].y)), "r"(__float_as_uint(v[5].x)), "r"(__float_as_uint(v[5].y)),
+        "r"(__float_as_uint(v[6].x)), "r"(__float_as_uint(v[6].y)), "r"(__float_as_uint(v[7].x)),
+        "r"(__float_as_uint(v[7].y))
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(__float_as_uint(v.x)),
+                 "r"(__float_as_uint(v.y))
+                 : "memory");
 }
 
-template <int NP, bool RING>
-__global__ void __launch_bounds__(kTmaThreads, 2) monitor_kernel_tma(const KParams prm) {
+// Shared-memory footprint of the TMA kernel (host mirror in bwm_capi.cu).
+__host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
+    return (int64_t)kStageRows * kRowBytes * (mode == kRingLag ? 2 : 1);
+}
+
+template <int NP, int MODE>
+__global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_tma(const KParams prm) {
     constexpr int SP = Coefs<NP>::SP;
     constexpr int R = kStageRows;
     constexpr int S = kStages;
-    constexpr int64_t SB = tma_stage_bytes(RING);
+    constexpr int64_t SB = tma_stage_bytes(MODE);
     constexpr int ROWF2 = kTile / 2;             // float2 per staged row
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
+    const int NA = (N + 3) & ~3;
     unsigned char* s_stage = smem_raw;                                   // [S][SB]
     float* s_mt = reinterpret_cast<float*>(smem_raw + S * SB);           // [n][SP]
     float* s_xt = s_mt + n * SP;                                         // [N][SP]
-    float* s_bd = s_xt + N * SP;                                         // [N-n] padded to 4
-    float2* s_ring = reinterpret_cast<float2*>(s_bd + ((N - n + 3) & ~3));   // [h][kThreads] (RING)
+    float* s_bd = s_xt + N * SP;                                         // [NA] bound by row t (t >= n)
+    float2* s_ring = reinterpret_cast<float2*>(s_bd + NA);               // [h][kThreads] (kRingSmem)
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(
-        reinterpret_cast<unsigned char*>(s_ring) + (RING ? (int64_t)h * kThreads * 8 : 0));
+        reinterpret_cast<unsigned char*>(s_ring) + (MODE == kRingSmem ? (int64_t)h * kThreads * 8 : 0));
     uint64_t* full = s_bar;          // [S]
     uint64_t* empty = s_bar + S;     // [S]
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * S);
 
     for (int i = threadIdx.x; i < n * SP; i += kTmaThreads) s_mt[i] = prm.mt[i];
     for (int i = threadIdx.x; i < N * SP; i += kTmaThreads) s_xt[i] = prm.xt[i];
-    for (int i = threadIdx.x; i < N - n; i += kTmaThreads) s_bd[i] = prm.bound[i];
+    for (int i = threadIdx.x; i < N - n; i += kTmaThreads) s_bd[n + i] = prm.bound[i];
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + s, 1);
@@ -91,34 +152,42 @@ __global__ void __launch_bounds__(kTmaThreads, 2) monitor_kernel_tma(const KPara
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (MODE == kRingTmem && threadIdx.x < 32) tmem_alloc(s_tmem, (uint32_t)prm.tmem_cols);
+    if (MODE == kRingTmem) tmem_fence_before();
     __syncthreads();
+    if (MODE == kRingTmem) tmem_fence_after();
 
     const int64_t n_tiles = prm.n_pixels / kTile;      // host guarantees whole tiles
     const int64_t ld = prm.ld_y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t3 = (n / R) * R;                        // first row of the aligned monitoring stream
 
     // =============================== producer ==========================================
     if (warp == kConsumerWarps) {
-        if (lane != 0) return;
-        uint32_t it = 0;
-        for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-            const float* yt = prm.y + tile * kTile;
-            for (int pass = 0; pass < 3; ++pass) {
-                const int lo = pass == 2 ? n : 0, hi = pass == 2 ? N : n;
-                const bool lag = !RING && pass == 2;
-                for (int r0 = lo; r0 < hi; r0 += R) {
-                    const int rows = min(R, hi - r0);
-                    const int s = it % S;
-                    mbar_wait(empty + s, ((it / S) & 1) ^ 1);
-                    mbar_expect_tx(full + s, (uint32_t)(rows * kRowBytes * (lag ? 2 : 1)));
-                    unsigned char* dst = s_stage + s * SB;
-                    for (int r = 0; r < rows; ++r)
-                        bulk_g2s(dst + r * kRowBytes, yt + (int64_t)(r0 + r) * ld, kRowBytes, full + s);
-                    if (lag)
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                const float* yt = prm.y + tile * kTile;
+                for (int pass = 0; pass < 3; ++pass) {
+                    const int lo = pass == 2 ? t3 : 0, hi = pass == 2 ? N : n;
+                    const bool lag = MODE == kRingLag && pass == 2;
+                    for (int r0 = lo; r0 < hi; r0 += R) {
+                        const int rows = min(R, hi - r0);
+                        const int s = it % S;
+                        mbar_wait(empty + s, ((it / S) & 1) ^ 1);
+                        // lag rows t-h < 0 only occur for skipped rows t < n: clamp their source
+                        int lag_lo = 0;
+                        if (lag) while (lag_lo < rows && r0 + lag_lo - h < 0) ++lag_lo;
+                        mbar_expect_tx(full + s, (uint32_t)((rows + (lag ? rows - lag_lo : 0)) * kRowBytes));
+                        unsigned char* dst = s_stage + s * SB;
                         for (int r = 0; r < rows; ++r)
-                            bulk_g2s(dst + (R + r) * kRowBytes, yt + (int64_t)(r0 + r - h) * ld, kRowBytes,
-                                     full + s);
-                    ++it;
+                            bulk_g2s(dst + r * kRowBytes, yt + (int64_t)(r0 + r) * ld, kRowBytes, full + s);
+                        if (lag)
+                            for (int r = lag_lo; r < rows; ++r)
+                                bulk_g2s(dst + (R + r) * kRowBytes, yt + (int64_t)(r0 + r - h) * ld, kRowBytes,
+                                         full + s);
+                        ++it;
+                    }
                 }
             }
         }
@@ -129,6 +198,9 @@ __global__ void __launch_bounds__(kTmaThreads, 2) monitor_kernel_tma(const KPara
     const int tid = threadIdx.x;
     float2* ring = s_ring + tid;
     const int wstart = n - h + 1;             // first row of MOSUM window 0 (mosum.py:59)
+    const int L = prm.ring_rows;
+    const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(warp * 32) << 16) : 0u;
+    auto tcol = [&](int row) -> uint32_t { return tbase + (uint32_t)(2 * row); };
     uint32_t it = 0;
     int cur = 0;
     auto acquire = [&]() -> const float2* {
@@ -199,8 +271,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) monitor_kernel_tma(const KPara
         // ---- pass 2: history residuals, sigma^2, MOSUM window 0 ----------------------
         float2 ss = f2(0.f, 0.f), acc = f2(0.f, 0.f);
         last = f2(0.f, 0.f);
-        float2 lag_last = f2(0.f, 0.f);          // !RING: fill state of the lagging cursor
-        int slot = wstart % h;                   // ring slot of row t is t mod h
+        float2 lag_last = f2(0.f, 0.f);          // kRingLag: fill state of the lagging cursor
+        int slot = wstart % h;                   // kRingSmem: slot of row t is t mod h
         for (int t0 = 0; t0 < n; t0 += R) {
             const float2* st = acquire();
             const int rows = min(R, n - t0);
@@ -211,78 +283,110 @@ __global__ void __launch_bounds__(kTmaThreads, 2) monitor_kernel_tma(const KPara
                     ss = fma2(r, r, ss);
                 }
             } else {
+                float2 rr[R];
+                if (MODE == kRingTmem && rows < R) {
+                    tmem_wait_st();
+                    tmem_ld16(tcol(t0 % L), rr);   // keep ring rows of t >= n (read-modify-write)
+                }
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     if (k < rows) {
                         const int t = t0 + k;
                         const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
                         ss = fma2(r, r, ss);
+                        rr[k] = r;
                         if (t >= wstart) {
                             acc = add2(acc, r);
-                            if (RING) {
+                            if (MODE == kRingSmem) {
                                 ring[slot * kThreads] = r;
                                 slot = (slot + 1 == h) ? 0 : slot + 1;
                             }
                         }
-                        if (!RING && t == wstart - 1) lag_last = last;
+                        if (MODE == kRingLag && t == wstart - 1) lag_last = last;
                     }
+                }
+                if (MODE == kRingTmem) {
+                    const int wb = t0 % L;
+                    tmem_st16(tcol(wb), rr);
+                    if (wb == 0) tmem_st16(tcol(L), rr);
                 }
             }
             release();
         }
-        if (RING) ring[slot * kThreads] = f2(0.f, 0.f);   // slot of r_{n-h}: not in window 0
+        // the ring slot of r_{n-h} must read as 0: window 0 does not contain it
+        if (MODE == kRingSmem) ring[slot * kThreads] = f2(0.f, 0.f);
+        if (MODE == kRingTmem) {
+            const int z = (n - h) % L;
+            tmem_st2(tcol(z), f2(0.f, 0.f));
+            if (z < R) tmem_st2(tcol(L + z), f2(0.f, 0.f));
+        }
 
-        // sigma (engine.py:363-371) and the zero-sigma contract (engine.py:373-378)
-        const bool z0 = valid0 && ss.x == 0.f, z1 = valid1 && ss.y == 0.f;
+        // sigma (engine.py:363-371) and the zero-sigma contract (engine.py:373-378): the
+        // reference raises when float64 gives sigma == 0 exactly — an identically zero
+        // history (c == 0).  A non-zero constant history has round-off sigma ~1e-17 there
+        // (MO ~1e15): sigma_scale 0 reproduces its decisions (any non-zero window crosses).
+        const bool z0 = valid0 && ss.x == 0.f && c.x == 0.f, z1 = valid1 && ss.y == 0.f && c.y == 0.f;
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
-        const float2 var = mul2(ss, f2(prm.inv_dof, prm.inv_dof));
-        float2 inv;
-        inv.x = (valid0 && ss.x > 0.f) ? 1.0f / (sqrtf(var.x) * prm.sqrt_n) : 0.f;
-        inv.y = (valid1 && ss.y > 0.f) ? 1.0f / (sqrtf(var.y) * prm.sqrt_n) : 0.f;
-        if (RING)
-            for (int s = 0; s < h; ++s) ring[s * kThreads] = mul2(ring[s * kThreads], inv);
-        acc = mul2(acc, inv);
-        float2 nbs[NP];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) nbs[i] = mul2(nb[i], inv);
+        const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);
 
-        // ---- pass 3: monitoring period, fused MOSUM + detect -------------------------
+        // ---- pass 3: monitoring period, fused MOSUM + detect (unscaled frame) ----------
         float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f);
         int first0 = 0x7fffffff, first1 = 0x7fffffff;
         float* const mo_out = prm.mosum;
-        auto mon_row = [&](const float2 v, const float2 lv, const int t, const bool past_n) {
-            const float2 r = dot_row<NP, SP>(mul2(fill(v, negc, last), inv), s_xt + t * SP, nbs);
-            float2 old = f2(0.f, 0.f);
-            if (RING) {
-                old = ring[slot * kThreads];
-                ring[slot * kThreads] = r;
-                slot = (slot + 1 == h) ? 0 : slot + 1;
-            } else if (past_n || t > n) {   // r_{t-h}; at t == n, r_{n-h} is outside window 0
-                old = dot_row<NP, SP>(mul2(fill(lv, negc, lag_last), inv), s_xt + (t - h) * SP, nbs);
-            }
-            acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
-            const int j = t - n;
-            const float b = s_bd[j];
-            const float a0 = fabsf(acc.x), a1 = fabsf(acc.y);
-            mx.x = fmaxf(mx.x, a0);
-            mx.y = fmaxf(mx.y, a1);
-            if (a0 > b) first0 = min(first0, j + 1);  // strict crossing (_kernels.py:47)
-            if (a1 > b) first1 = min(first1, j + 1);
-            msum = add2(msum, acc);
-            if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)j * prm.ld_out + px0) = acc;
-        };
-        for (int t0 = n; t0 < N; t0 += R) {
+        const float2 inv = inv_scale(sc);
+        for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
-            const float2* lst = st + R * ROWF2;          // lag rows (!RING)
-            const int rows = min(R, N - t0);
-            if (rows == R && t0 > n) {
+            const float2* lst = st + R * ROWF2;          // lag rows (kRingLag)
+            const bool full_stage = t0 > n && t0 + R <= N;
+            float2 oldv[R], newv[R];
+            if (MODE == kRingTmem) {
+                tmem_wait_st();
+                const int rb = ((t0 - h) % L + L) % L;
+                tmem_ld16(tcol(rb), oldv);
+                if (!full_stage) tmem_ld16(tcol(t0 % L), newv);   // preserve rows t < n
+            }
+            float4 b4[R / 4];
 #pragma unroll
-                for (int k = 0; k < R; ++k)
-                    mon_row(st[k * ROWF2], RING ? f2(0.f, 0.f) : lst[k * ROWF2], t0 + k, true);
+            for (int q = 0; q < R / 4; ++q) b4[q] = reinterpret_cast<const float4*>(s_bd + t0)[q];
+            auto row = [&](const int k, const bool checked) {
+                const int t = t0 + k;
+                if (checked && (t < n || t >= N)) return;
+                const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+                float2 old = f2(0.f, 0.f);
+                if (MODE == kRingTmem) {
+                    old = oldv[k];
+                    newv[k] = r;
+                } else if (MODE == kRingSmem) {
+                    old = ring[slot * kThreads];
+                    ring[slot * kThreads] = r;
+                    slot = (slot + 1 == h) ? 0 : slot + 1;
+                } else if (!checked || t > n) {          // r_{t-h}; r_{n-h} is outside window 0
+                    old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
+                }
+                acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
+                const float bj = (k & 3) == 0 ? b4[k >> 2].x : (k & 3) == 1 ? b4[k >> 2].y
+                               : (k & 3) == 2 ? b4[k >> 2].z : b4[k >> 2].w;
+                const float2 bs = mul2(sc, f2(bj, bj));   // boundary in the unscaled frame
+                const float a0 = fabsf(acc.x), a1 = fabsf(acc.y);
+                mx.x = fmaxf(mx.x, a0);
+                mx.y = fmaxf(mx.y, a1);
+                const int j1 = t - n + 1;
+                if (a0 > bs.x) first0 = min(first0, j1);  // strict crossing (_kernels.py:47)
+                if (a1 > bs.y) first1 = min(first1, j1);
+                msum = add2(msum, acc);
+                if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)(t - n) * prm.ld_out + px0) = mul2(acc, inv);
+            };
+            if (full_stage) {
+#pragma unroll
+                for (int k = 0; k < R; ++k) row(k, false);
             } else {
 #pragma unroll
-                for (int k = 0; k < R; ++k)
-                    if (k < rows) mon_row(st[k * ROWF2], RING ? f2(0.f, 0.f) : lst[k * ROWF2], t0 + k, false);
+                for (int k = 0; k < R; ++k) row(k, true);
+            }
+            if (MODE == kRingTmem) {
+                const int wb = t0 % L;
+                tmem_st16(tcol(wb), newv);
+                if (wb == 0) tmem_st16(tcol(L), newv);
             }
             release();
         }
@@ -293,8 +397,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) monitor_kernel_tma(const KPara
             *reinterpret_cast<uchar2*>(prm.valid + px0) = make_uchar2(valid0, valid1);
             *reinterpret_cast<int2*>(prm.first_idx + px0) =
                 make_int2(first0 == 0x7fffffff ? 0 : first0, first1 == 0x7fffffff ? 0 : first1);
-            *reinterpret_cast<float2*>(prm.max_abs + px0) = mx;
-            if (prm.mo_mean) *reinterpret_cast<float2*>(prm.mo_mean + px0) = mul2(msum, f2(inv_m, inv_m));
+            *reinterpret_cast<float2*>(prm.max_abs + px0) = mul2(mx, inv);
+            if (prm.mo_mean) *reinterpret_cast<float2*>(prm.mo_mean + px0) = mul2(mul2(msum, inv), f2(inv_m, inv_m));
             if (prm.beta) {
                 // back to the raw basis (bwm.h): b0 = c + b0' - b1' tc/ts, b1 = b1'/ts
                 float2 bo[NP];
@@ -309,6 +413,14 @@ __global__ void __launch_bounds__(kTmaThreads, 2) monitor_kernel_tma(const KPara
                         f2(valid0 ? bo[i].x : 0.f, valid1 ? bo[i].y : 0.f);
             }
         }
+    }
+
+    if (MODE == kRingTmem) {
+        tmem_wait_st();
+        tmem_fence_before();
+        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");   // consumer warps only
+        tmem_fence_after();
+        if (warp == 0) tmem_dealloc(*s_tmem, (uint32_t)prm.tmem_cols);
     }
 }
 

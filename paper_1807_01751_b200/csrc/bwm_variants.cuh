@@ -8,15 +8,20 @@ enum Kind { kLdgFast = 0, kLdgSafe = 1, kTma = 2 };
 using KernelFn = void (*)(const KParams);
 }  // namespace bwm
 
-// Defines bwm::KernelFn bwm_pick_p<NP>(int kind, bool ring) in the including TU.
+// Defines bwm::KernelFn bwm_pick_p<NP>(int kind, int mode) in the including TU.
+// mode: bwm::RingMode (kRingSmem / kRingTmem / kRingLag); the LDG kernels have a shared-memory
+// ring (any mode but kRingLag) or the lagging cursor.
 #define BWM_DEFINE_PICK(NP)                                                                      \
-    bwm::KernelFn bwm_pick_p##NP(int kind, bool ring) {                                          \
+    bwm::KernelFn bwm_pick_p##NP(int kind, int mode) {                                           \
+        const bool ring = mode != bwm::kRingLag;                                                 \
         switch (kind) {                                                                          \
             case bwm::kLdgFast:                                                                  \
                 return ring ? bwm::monitor_kernel_ldg<NP, false, true> : bwm::monitor_kernel_ldg<NP, false, false>; \
             case bwm::kLdgSafe:                                                                  \
                 return ring ? bwm::monitor_kernel_ldg<NP, true, true> : bwm::monitor_kernel_ldg<NP, true, false>;   \
             default:                                                                             \
-                return ring ? bwm::monitor_kernel_tma<NP, true> : bwm::monitor_kernel_tma<NP, false>; \
+                return mode == bwm::kRingSmem ? bwm::monitor_kernel_tma<NP, bwm::kRingSmem>      \
+                     : mode == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem>      \
+                                              : bwm::monitor_kernel_tma<NP, bwm::kRingLag>;      \
         }                                                                                        \
     }

@@ -7,6 +7,13 @@ outputs and the CPU oracle.  Tolerances (BASELINE.json north_star, SURVEY.md §8
   max_abs_mo   rtol 1e-4
   mosum_mean   |d| <= 1e-4 * max(|mean_ref|, max_abs_ref)  (a mean of signed terms)
   beta         |d_i| <= 1e-4 |beta_ref,i| + 1e-4 ||M_i,:||_1 ||y_hist||_inf
+
+Degenerate pixels — a constant filled history (e.g. a leading gap covering the history) —
+have sigma at float64 round-off in the reference: its MO is round-off / round-off (noise) on
+windows without a real value change, and ~1e15 on windows with one.  The kernel computes
+sigma = 0 exactly there.  Magnitudes are not compared; where the reference blew up
+(max |MO| > 1e10) both must have blown up and agree on the first break; a constant whole
+series (noise-only decisions in the reference) is excluded.
 """
 
 import numpy as np
@@ -26,18 +33,29 @@ def _pkg():
     return pkg
 
 
+def degenerate_pixels(case):
+    filled, valid = bo.fill_block(case.y)
+    return valid & (filled[:case.n] == filled[0]).all(axis=0)
+
+
 def check_parity(case, first_break, max_abs, valid, mean=None, beta=None, mosum=None):
     n_mon = case.y.shape[0] - case.n
     P = case.y.shape[1]
     assert np.array_equal(valid, case.valid), "valid mask differs"
     first_gpu = np.where(first_break > 0, first_break - case.n, 0)
     border = bo.borderline_from_pairs(case.near, n_mon, P, case.first_idx, first_gpu)
+    degen = degenerate_pixels(case)
+    blown = degen & (case.max_abs_mo > 1e10)
+    border |= degen & ~blown
     bad = np.flatnonzero((first_gpu != case.first_idx) & ~border)
     assert bad.size == 0, f"{case.name}: {bad.size} non-borderline break mismatches, e.g. {bad[:5]}"
-    np.testing.assert_allclose(max_abs, case.max_abs_mo, rtol=RTOL, atol=0)
+    assert np.all(max_abs[blown] > 1e10), "round-off-sigma pixels must blow up where the reference does"
+    assert degen.sum() <= max(12, P // 100), "degenerate pixels must stay rare in the fixtures"
+    ok = ~degen
+    np.testing.assert_allclose(max_abs[ok], case.max_abs_mo[ok], rtol=RTOL, atol=0)
     if mean is not None:
         scale = np.maximum(np.abs(case.mosum_mean), case.max_abs_mo)
-        assert np.all(np.abs(mean - case.mosum_mean) <= RTOL * scale + 1e-30)
+        assert np.all((np.abs(mean - case.mosum_mean) <= RTOL * scale + 1e-30)[ok])
     if beta is not None and case.beta is not None:
         X = bo.design_matrix(case.t, case.freq, case.k)
         M = bo.mapping_matrix(X, case.n)
@@ -47,7 +65,7 @@ def check_parity(case, first_break, max_abs, valid, mean=None, beta=None, mosum=
         assert np.all(np.abs(beta - case.beta) <= tol), f"{case.name}: beta out of tolerance"
     if mosum is not None and case.mosum is not None:
         scale = np.maximum(case.max_abs_mo, 1e-30)[None, :]
-        assert np.all(np.abs(mosum - case.mosum) <= RTOL * scale)
+        assert np.all((np.abs(mosum - case.mosum) <= RTOL * scale)[:, ok])
     return int(border.sum())
 
 
