@@ -306,7 +306,7 @@ def run_ours(args):
                        "parallelism": f"pixel tiles, {world} rank(s), no collective on the data path"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "bytes_per_pixel": bpp, "kernel_ms": k_avg},
+                         "bytes_per_pixel": bpp, "kernel_ms": k_avg, "launch": plan.info()},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),

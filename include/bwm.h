@@ -20,9 +20,12 @@
  *   - return 0 on success, a negative BWM_E* code for invalid arguments, or a positive
  *     cudaError_t value for CUDA failures; bwm_last_error() holds the message (per thread).
  *
- * The constant tables (mapping, design, boundary) are host setup in float64 — exactly
- * the reference's build_design_matrix / fit_mapping / boundary_values
- * (model.py:90-152, mosum.py:68-79) — and are handed over once through bwm_plan_create.
+ * The constant tables (design, boundary) are host setup in float64 — the reference's
+ * build_design_matrix / boundary_values (model.py:90-110, mosum.py:68-79) — handed over once
+ * through bwm_plan_create.  The library solves the history least squares itself: a float64
+ * QR of the history design gives an orthonormal basis Q (the role of fit_mapping's
+ * M = (X_h X_h^T)^-1 X_h, model.py:118-152), so that beta_Q = Q^T y_h and the residual sum of
+ * squares is ||y_h||^2 - ||beta_Q||^2 without a second sweep over the history.
  */
 #ifndef BWM_H
 #define BWM_H
@@ -34,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BWM_ABI_VERSION 1
+#define BWM_ABI_VERSION 2
 
 /* error codes (negative); positive returns are cudaError_t values */
 #define BWM_OK 0
@@ -61,7 +64,6 @@ typedef struct bwm_dims {
  * conditioned.  Beta is reported back in the reference's raw basis.
  */
 typedef struct bwm_tables {
-    const double* mapping;   /* [p][n]  M' = (X'_h X'_h^T)^-1 X'_h (centred basis)         */
     const double* design;    /* [p][N]  X'  rows: 1, (t-tc)/ts, sin(2pi j t/f), cos(...)    */
     const double* bound;     /* [N-n]   crit * sqrt(log_plus((n+1+j)/n))  (mosum.py:68-79)  */
     double trend_center;     /* tc */
@@ -114,6 +116,22 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
    H2D/D2H byte counts.  For PhaseTimings. */
 int bwm_last_host_stats(const bwm_plan* plan, double* kernel_ms, double* total_ms,
                         int64_t* h2d_bytes, int64_t* d2h_bytes);
+
+/* Launch configuration a plan chose (diagnostics; bench.py reports it). */
+typedef struct bwm_plan_info_t {
+    int32_t ring_mode;        /* TMA kernel residual ring: 0 smem, 1 tensor memory, 2 lagging cursor */
+    int32_t ring_rows;        /* TMEM ring rows L (0 unless ring_mode == 1)                          */
+    int32_t tmem_cols;        /* TMEM columns allocated per CTA                                      */
+    int32_t sms;              /* streaming multiprocessors of the device                             */
+    int64_t smem_tma;         /* dynamic shared memory per CTA, TMA kernel (0: not usable)           */
+    int64_t smem_ldg;         /* dynamic shared memory per CTA, LDG kernels                          */
+    int32_t ctas_per_sm_tma;  /* persistent CTAs per SM, TMA kernel                                  */
+    int32_t ctas_per_sm_ldg;  /* persistent CTAs per SM, LDG kernel                                  */
+    int32_t occupancy_tma;    /* occupancy-API result for the TMA kernel                             */
+    int32_t force_ldg;        /* BWM_KERNEL=ldg was set at plan creation                             */
+} bwm_plan_info_t;
+
+int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info);
 
 /* Number of bwm kernel launches issued by this process so far (all plans). */
 int64_t bwm_launch_count(void);

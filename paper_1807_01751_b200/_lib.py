@@ -34,7 +34,6 @@ class Dims(C.Structure):
 
 class Tables(C.Structure):
     _fields_ = [
-        ("mapping", C.POINTER(C.c_double)),
         ("design", C.POINTER(C.c_double)),
         ("bound", C.POINTER(C.c_double)),
         ("trend_center", C.c_double),
@@ -55,6 +54,14 @@ class Outputs(C.Structure):
     ]
 
 
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("ring_mode", C.c_int32), ("ring_rows", C.c_int32), ("tmem_cols", C.c_int32), ("sms", C.c_int32),
+        ("smem_tma", C.c_int64), ("smem_ldg", C.c_int64), ("ctas_per_sm_tma", C.c_int32),
+        ("ctas_per_sm_ldg", C.c_int32), ("occupancy_tma", C.c_int32), ("force_ldg", C.c_int32),
+    ]
+
+
 # (name, restype, argtypes) — every symbol include/bwm.h declares
 SIGNATURES = [
     ("bwm_plan_create", C.c_int, [C.POINTER(Dims), C.POINTER(Tables), C.c_int, C.POINTER(C.c_void_p)]),
@@ -65,6 +72,7 @@ SIGNATURES = [
      [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Outputs)]),
     ("bwm_last_host_stats", C.c_int,
      [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("bwm_plan_info", C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
     ("bwm_launch_count", C.c_int64, []),
     ("bwm_smem_bytes", C.c_int64, [C.POINTER(Dims)]),
     ("bwm_last_error", C.c_char_p, []),
@@ -90,7 +98,7 @@ def load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.bwm_abi_version() != 1:
+    if lib.bwm_abi_version() != 2:
         raise RuntimeError("libbwm ABI version mismatch; rebuild the library")
     _lib = lib
     return lib

@@ -77,16 +77,18 @@ TmaRing tma_ring_for(int h) {
         while (cols < need) cols *= 2;
         return {bwm::kRingTmem, L, cols};
     }
-    return {h < 8 ? (int)bwm::kRingSmem : (int)bwm::kRingLag, 0, 0};
+    return {h < 8 ? -1 : (int)bwm::kRingLag, 0, 0};   // -1: no TMA variant (LDG kernel)
 }
 
-// shared memory of the TMA kernel: stages + tables (bound indexed by row) + smem ring
-// (kRingSmem only) + 2*kStages mbarriers + the TMEM address slot
+// shared memory of the TMA kernel: stages + tables (mapping padded to 8-row stages, bound
+// indexed by row) + 2*kStages mbarriers + the TMEM address slot; 0 when no TMA variant applies
 int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
+    (void)h;
+    if (mode < 0) return 0;
     const int sp = (p + 3) & ~3;
-    int64_t fl = (int64_t)n * sp + (int64_t)N * sp + ((N + 3) & ~3);
+    const int n8 = ((n + bwm::kStageRows - 1) / bwm::kStageRows) * bwm::kStageRows;
+    int64_t fl = (int64_t)n8 * sp + (int64_t)N * sp + ((N + 3) & ~3);
     int64_t bytes = bwm::kStages * bwm::tma_stage_bytes(mode) + fl * 4;
-    if (mode == bwm::kRingSmem) bytes += (int64_t)h * bwm::kThreads * 8;
     return bytes + 2 * bwm::kStages * 8 + 16;
 }
 
@@ -154,6 +156,7 @@ struct bwm_plan {
     float* d_mt = nullptr;
     float* d_xt = nullptr;
     float* d_bound = nullptr;
+    float* d_rinv = nullptr;
     float inv_dof = 0, sqrt_n = 0, tc_ts = 0, inv_ts = 0;
     bool ring = true;                  // LDG kernels: smem ring (else lagging cursor)
     TmaRing tring{};                   // TMA kernel ring mode
@@ -161,6 +164,7 @@ struct bwm_plan {
     int64_t smem_tma = 0;              // TMA kernel (0: does not fit -> LDG kernels only)
     int sms = 0;
     int blocks_per_sm[3] = {0, 0, 0};  // [Kind]
+    int occ_raw[3] = {0, 0, 0};        // occupancy API result before the TMEM cap
     bool force_ldg = false;            // BWM_KERNEL=ldg (A/B against the TMA kernel)
     HostPipe pipe;
     std::mutex mu;                     // serialises bwm_monitor_host on one plan
@@ -192,8 +196,8 @@ int64_t bwm_smem_bytes(const bwm_dims* d) {
     int rc = validate_dims(d);
     if (rc) return rc;
     const bool ring = d->bandwidth <= kRingMaxH;
-    (void)ring;
-    return smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, tma_ring_for(d->bandwidth).mode);
+    const int64_t tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, tma_ring_for(d->bandwidth).mode);
+    return tma > 0 ? tma : smem_bytes_for(d->n_obs, d->n_hist, d->bandwidth, d->n_params, ring);
 }
 
 int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_plan** out_plan) {
@@ -201,8 +205,8 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     *out_plan = nullptr;
     int rc = validate_dims(dims);
     if (rc) return rc;
-    if (!tb || !tb->mapping || !tb->design || !tb->bound)
-        return set_err(BWM_E_NULL, "tables (mapping, design, bound) must be non-NULL");
+    if (!tb || !tb->design || !tb->bound)
+        return set_err(BWM_E_NULL, "tables (design, bound) must be non-NULL");
     if (!(tb->trend_scale > 0) || !std::isfinite(tb->trend_center))
         return set_err(BWM_E_DIMS, "trend_scale must be positive and trend_center finite");
 
@@ -229,7 +233,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     int max_optin = 0;
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device);
-    if (plan->smem_tma > max_optin) plan->smem_tma = 0;
+    if (plan->smem_tma > max_optin || plan->tring.mode < 0) plan->smem_tma = 0;
     if (plan->smem > max_optin) {
         int64_t need = plan->smem;
         delete plan;
@@ -237,18 +241,56 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
                        (long long)need, max_optin);
     }
 
-    // float32 tables, transposed so one date's coefficients are contiguous (LDS.128)
-    std::vector<float> mt((size_t)n * sp, 0.f), xt((size_t)N * sp, 0.f), bd((size_t)(N - n));
-    for (int i = 0; i < p; ++i) {
-        for (int t = 0; t < n; ++t) mt[(size_t)t * sp + i] = (float)tb->mapping[(size_t)i * n + t];
-        for (int t = 0; t < N; ++t) xt[(size_t)t * sp + i] = (float)tb->design[(size_t)i * N + t];
+    // History least squares, float64: thin QR of the centred history design X'_h^T = Q R
+    // (modified Gram-Schmidt, two passes).  Q^T y_h are the coefficients in an orthonormal
+    // basis (so RSS = ||y_h||^2 - ||Q^T y_h||^2 in one sweep), Z = R^-T X' maps them to fitted
+    // values for every date, and R^-1 maps them back to beta' for the beta output.
+    std::vector<double> Q((size_t)n * p), Rm((size_t)p * p, 0.0);
+    for (int j = 0; j < p; ++j) {
+        for (int t = 0; t < n; ++t) Q[(size_t)t * p + j] = tb->design[(size_t)j * N + t];
+        for (int pass = 0; pass < 2; ++pass)
+            for (int i = 0; i < j; ++i) {
+                double d = 0.0;
+                for (int t = 0; t < n; ++t) d += Q[(size_t)t * p + i] * Q[(size_t)t * p + j];
+                Rm[(size_t)i * p + j] += d;
+                for (int t = 0; t < n; ++t) Q[(size_t)t * p + j] -= d * Q[(size_t)t * p + i];
+            }
+        double nrm = 0.0;
+        for (int t = 0; t < n; ++t) nrm += Q[(size_t)t * p + j] * Q[(size_t)t * p + j];
+        nrm = std::sqrt(nrm);
+        if (!(nrm > 1e-12)) {
+            delete plan;
+            return set_err(BWM_E_DIMS, "history design is rank deficient (column %d)", j);
+        }
+        Rm[(size_t)j * p + j] = nrm;
+        for (int t = 0; t < n; ++t) Q[(size_t)t * p + j] /= nrm;
     }
+    std::vector<double> Rinv((size_t)p * p, 0.0);          // upper triangular
+    for (int col = 0; col < p; ++col)
+        for (int i = col; i >= 0; --i) {
+            double v = (i == col) ? 1.0 : 0.0;
+            for (int k = i + 1; k <= col; ++k) v -= Rm[(size_t)i * p + k] * Rinv[(size_t)k * p + col];
+            Rinv[(size_t)i * p + col] = v / Rm[(size_t)i * p + i];
+        }
+    // float32 tables, transposed so one date's coefficients are contiguous (LDS.128)
+    std::vector<float> mt((size_t)n * sp, 0.f), xt((size_t)N * sp, 0.f), bd((size_t)(N - n)),
+        ri((size_t)p * p);
+    for (int t = 0; t < n; ++t)
+        for (int i = 0; i < p; ++i) mt[(size_t)t * sp + i] = (float)Q[(size_t)t * p + i];
+    for (int t = 0; t < N; ++t)
+        for (int i = 0; i < p; ++i) {      // z_t = R^-T x_t  <=>  z_t,i = sum_k Rinv[k][i] x_k,t
+            double z = 0.0;
+            for (int k = 0; k <= i; ++k) z += Rinv[(size_t)k * p + i] * tb->design[(size_t)k * N + t];
+            xt[(size_t)t * sp + i] = (float)z;
+        }
     for (int j = 0; j < N - n; ++j) bd[j] = (float)tb->bound[j];
+    for (size_t i = 0; i < ri.size(); ++i) ri[i] = (float)Rinv[i];
 
     auto fail = [&](cudaError_t e, const char* what) {
         cudaFree(plan->d_mt);
         cudaFree(plan->d_xt);
         cudaFree(plan->d_bound);
+        cudaFree(plan->d_rinv);
         delete plan;
         return set_err((int)e, "%s: %s", what, cudaGetErrorString(e));
     };
@@ -263,21 +305,47 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         return fail(e, "cudaMemcpy");
     if ((e = cudaMemcpy(plan->d_bound, bd.data(), bd.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
+    if ((e = cudaMalloc(&plan->d_rinv, ri.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMemcpy(plan->d_rinv, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy");
 
     for (int v = 0; v < 3; ++v) {
         const Kind kind = (Kind)v;
         const int64_t sm = kind == kTma ? plan->smem_tma : plan->smem;
         if (kind == kTma && sm == 0) continue;
         KernelFn fn = pick(p, kind, kind == kTma ? plan->tring.mode : (plan->ring ? 0 : (int)bwm::kRingLag));
+        // the limit is per-kernel global state shared by every plan: set it to the device
+        // maximum once, never lower it (a later plan must not shrink an earlier plan's launch)
         if ((e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sm)) != cudaSuccess)
+                                      max_optin)) != cudaSuccess)
             return fail(e, "cudaFuncSetAttribute");
         int nb = 0;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, threads_of(kind),
                                                                (size_t)sm)) != cudaSuccess)
             return fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-        if (kind == kTma && plan->tring.mode == bwm::kRingTmem)
-            nb = std::min(nb, 512 / plan->tring.cols);   // TMEM columns per SM
+        if (kind == kTma && plan->tring.mode == bwm::kRingTmem) {
+            // The occupancy API assumes a kernel that allocates Tensor Memory owns the SM's
+            // TMEM (reports 1).  Allocation is dynamic (tcgen05.alloc + relinquish_alloc_permit),
+            // so residency is bounded by registers, shared memory, threads and our own column
+            // budget: 512 columns per SM / tmem_cols per CTA.
+            cudaFuncAttributes fa{};
+            if ((e = cudaFuncGetAttributes(&fa, (const void*)fn)) != cudaSuccess)
+                return fail(e, "cudaFuncGetAttributes");
+            int regs_per_sm = 0, smem_per_sm = 0, reserved = 0, max_threads = 0;
+            cudaDeviceGetAttribute(&regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, device);
+            cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+            cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+            cudaDeviceGetAttribute(&max_threads, cudaDevAttrMaxThreadsPerMultiProcessor, device);
+            const int thr = threads_of(kind);
+            const int warps = (thr + 31) / 32;
+            const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;     // per-warp allocation unit
+            const int by_regs = regs_per_sm / (regs_warp * warps);
+            const int by_smem = (int)(smem_per_sm / (sm + (int64_t)fa.sharedSizeBytes + reserved));
+            const int by_thr = max_threads / thr;
+            const int by_tmem = 512 / plan->tring.cols;
+            nb = std::min(std::min(by_regs, by_smem), std::min(by_thr, by_tmem));
+        }
+        plan->occ_raw[v] = nb;
         plan->blocks_per_sm[v] = std::max(nb, 1);
     }
     *out_plan = plan;
@@ -314,6 +382,7 @@ void bwm_plan_destroy(bwm_plan* plan) {
     cudaFree(plan->d_mt);
     cudaFree(plan->d_xt);
     cudaFree(plan->d_bound);
+    cudaFree(plan->d_rinv);
     delete plan;
 }
 
@@ -347,6 +416,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     k.mt = plan->d_mt;
     k.xt = plan->d_xt;
     k.bound = plan->d_bound;
+    k.rinv = plan->d_rinv;
     k.inv_dof = plan->inv_dof;
     k.sqrt_n = plan->sqrt_n;
     k.ring_rows = plan->tring.rows;
@@ -541,6 +611,21 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
     hp.last_total_ms = total;
     hp.last_h2d = h2d;
     hp.last_d2h = d2h;
+    return BWM_OK;
+}
+
+int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {
+    if (!plan || !info) return set_err(BWM_E_NULL, "plan/info is NULL");
+    info->ring_mode = plan->tring.mode;
+    info->ring_rows = plan->tring.rows;
+    info->tmem_cols = plan->tring.cols;
+    info->smem_tma = plan->smem_tma;
+    info->smem_ldg = plan->smem;
+    info->ctas_per_sm_tma = plan->blocks_per_sm[kTma];
+    info->ctas_per_sm_ldg = plan->blocks_per_sm[kLdgFast];
+    info->occupancy_tma = plan->occ_raw[kTma];
+    info->sms = plan->sms;
+    info->force_ldg = plan->force_ldg ? 1 : 0;
     return BWM_OK;
 }
 

@@ -24,8 +24,9 @@ struct KParams {
     int64_t n_pixels;
     int64_t pixel_offset;       // global index of pixel 0 (zero-sigma reporting)
     int N, n, h, sp;            // sp: padded row stride of the coefficient tables
-    const float* mt;            // [n][sp]  M'^T  (row t = coefficients of date t)
-    const float* xt;            // [N][sp]  X'^T
+    const float* mt;            // [n][sp]  Q^T: orthonormal history basis, row t = date t
+    const float* xt;            // [N][sp]  Z^T = (R^-T X')^T: fitted value = z_t . beta_Q
+    const float* rinv;          // [p][p]   R^-1 (row-major): beta' = R^-1 beta_Q (beta output)
     const float* bound;         // [N-n]
     float inv_dof;              // 1 / (n - p)
     float sqrt_n;
@@ -106,6 +107,48 @@ __device__ __forceinline__ void axpy_row(float2 (&part)[NP], float2 vc, const fl
         if (4 * q + 1 < NP) part[4 * q + 1] = fma2s(vc, m.y, part[4 * q + 1]);
         if (4 * q + 2 < NP) part[4 * q + 2] = fma2s(vc, m.z, part[4 * q + 2]);
         if (4 * q + 3 < NP) part[4 * q + 3] = fma2s(vc, m.w, part[4 * q + 3]);
+    }
+}
+
+// Residual sum of squares of the history fit in the orthonormal basis (one pass):
+// RSS = ||y_h - c||^2 - ||beta_Q||^2, accumulated in float64 (q from 16-date float32 block
+// partials).  Clamped at 0: a (near-)exact fit is a zero-sigma pixel.
+template <int NP>
+__device__ __forceinline__ float2 rss_onepass(double q0, double q1, const float2 (&bq)[NP]) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        s0 = fma((double)bq[i].x, (double)bq[i].x, s0);
+        s1 = fma((double)bq[i].y, (double)bq[i].y, s1);
+    }
+    return f2((float)fmax(q0 - s0, 0.0), (float)fmax(q1 - s1, 0.0));
+}
+
+// beta' = R^-1 beta_Q (centred basis), then the raw basis of the reference (bwm.h):
+// b0 = c + b0' - b1' tc/ts, b1 = b1'/ts.  Invalid pixels report 0.
+template <int NP>
+__device__ __forceinline__ void store_beta(const KParams& prm, int64_t px0, float2 c, const float2 (&bq)[NP],
+                                           bool v0, bool v1, int npx) {
+    float2 bo[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        float2 a = f2(0.f, 0.f);
+#pragma unroll
+        for (int j = i; j < NP; ++j) a = fma2s(bq[j], __ldg(prm.rinv + i * NP + j), a);   // R^-1 upper triangular
+        bo[i] = a;
+    }
+    const float2 b1 = bo[1];
+    bo[0] = add2(c, sub2(bo[0], mul2(b1, f2(prm.tc_ts, prm.tc_ts))));
+    bo[1] = mul2(b1, f2(prm.inv_ts, prm.inv_ts));
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        float* o = prm.beta + (int64_t)i * prm.ld_out + px0;
+        if (npx >= 2 && (reinterpret_cast<uintptr_t>(o) & 7) == 0) {
+            *reinterpret_cast<float2*>(o) = f2(v0 ? bo[i].x : 0.f, v1 ? bo[i].y : 0.f);
+        } else {
+            if (npx >= 1) o[0] = v0 ? bo[i].x : 0.f;
+            if (npx >= 2) o[1] = v1 ? bo[i].y : 0.f;
+        }
     }
 }
 

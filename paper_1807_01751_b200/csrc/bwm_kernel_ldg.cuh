@@ -101,19 +101,23 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         float2 hi[NP], lo[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) { hi[i] = f2(0.f, 0.f); lo[i] = f2(0.f, 0.f); }
+        double q0 = 0.0, q1 = 0.0;           // ||y - c||^2 (16-date float32 partials, float64 sum)
         float2 last = f2(0.f, 0.f);
         const float* pf = yp + (int64_t)D * ld;   // refill target of the row being consumed
         for (int t0 = 0; t0 < n; t0 += D) {
             float2 part[NP];
 #pragma unroll
             for (int i = 0; i < NP; ++i) part[i] = f2(0.f, 0.f);
+            float2 qpart = f2(0.f, 0.f);
             if (t0 + 2 * D <= n) {
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
                     const float2 v = buf[k];
                     buf[k] = ldp<SAFE>(pf, npx);
                     pf += ld;
-                    axpy_row<NP, SP>(part, fill(v, negc, last), s_mt + (t0 + k) * SP);
+                    const float2 vc = fill(v, negc, last);
+                    axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
+                    qpart = fma2(vc, vc, qpart);
                 }
             } else {
 #pragma unroll
@@ -124,7 +128,9 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                         if (t + D < n) buf[k] = ldp<SAFE>(pf, npx);        // next pass-1 row
                         else if (k < N) buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);  // pass-2 row k
                         pf += ld;
-                        axpy_row<NP, SP>(part, fill(v, negc, last), s_mt + t * SP);
+                        const float2 vc = fill(v, negc, last);
+                        axpy_row<NP, SP>(part, vc, s_mt + t * SP);
+                        qpart = fma2(vc, vc, qpart);
                     } else if (k < N) {
                         buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);      // free slot: pass-2 row k
                     }
@@ -132,13 +138,16 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
             }
 #pragma unroll
             for (int i = 0; i < NP; ++i) two_sum(hi[i], lo[i], part[i]);
+            q0 += (double)qpart.x;
+            q1 += (double)qpart.y;
         }
-        float2 nb[NP];    // -beta'
+        float2 bq[NP], nb[NP];    // beta_Q and -beta_Q
 #pragma unroll
-        for (int i = 0; i < NP; ++i) { const float2 b = add2(hi[i], lo[i]); nb[i] = f2(-b.x, -b.y); }
+        for (int i = 0; i < NP; ++i) { bq[i] = add2(hi[i], lo[i]); nb[i] = f2(-bq[i].x, -bq[i].y); }
+        const float2 ss = rss_onepass<NP>(q0, q1, bq);
 
-        // ---- pass 2: history residuals, sigma^2, MOSUM window 0 ----------------------
-        float2 ss = f2(0.f, 0.f), acc = f2(0.f, 0.f);
+        // ---- pass 2: fill state through the history; residuals of window 0 --------------
+        float2 acc = f2(0.f, 0.f);
         last = f2(0.f, 0.f);
         float2 lag_last = f2(0.f, 0.f);          // !RING: fill state of the lagging cursor
         float2 lbuf[RING ? 1 : D];               // !RING: prefetched rows t+D-h
@@ -151,8 +160,7 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                     const float2 v = buf[k];
                     buf[k] = ldp<SAFE>(pf, npx);
                     pf += ld;
-                    const float2 r = dot_row<NP, SP>(fill(v, negc, last), s_xt + (t0 + k) * SP, nb);
-                    ss = fma2(r, r, ss);
+                    fill(v, negc, last);        // rows before window 0: fill state only
                 }
             } else {
 #pragma unroll
@@ -164,9 +172,9 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                         else if (has_next && k < n) buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);
                         if (!RING && t + D > n && t + D < N) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
                         pf += ld;
-                        const float2 r = dot_row<NP, SP>(fill(v, negc, last), s_xt + t * SP, nb);
-                        ss = fma2(r, r, ss);
+                        const float2 vc = fill(v, negc, last);
                         if (t >= wstart) {
+                            const float2 r = dot_row<NP, SP>(vc, s_xt + t * SP, nb);
                             acc = add2(acc, r);
                             if (RING) {
                                 ring[slot * kThreads] = r;
@@ -257,26 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                 prm.max_abs[px0 + 1] = mxs.y;
                 if (prm.mo_mean) prm.mo_mean[px0 + 1] = mean.y;
             }
-            if (prm.beta) {
-                // back to the raw basis (bwm.h): b0 = c + b0' - b1' tc/ts, b1 = b1'/ts
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    if (e < npx) {
-                        const bool ok = e == 0 ? valid0 : valid1;
-                        const float ce = e == 0 ? c.x : c.y;
-                        const float b1 = e == 0 ? -nb[1].x : -nb[1].y;
-                        float* o = prm.beta + px0 + e;
-#pragma unroll
-                        for (int i = 0; i < NP; ++i) {
-                            const float bi = e == 0 ? -nb[i].x : -nb[i].y;
-                            float val = bi;
-                            if (i == 0) val = ce + (bi - b1 * prm.tc_ts);
-                            if (i == 1) val = bi * prm.inv_ts;
-                            o[(int64_t)i * prm.ld_out] = ok ? val : 0.f;
-                        }
-                    }
-                }
-            }
+            if (prm.beta) store_beta<NP>(prm, px0, c, bq, valid0, valid1, npx);
         }
 
         if (!has_next) break;

@@ -9,10 +9,15 @@
 // per-pixel pipeline state; bytes in flight per SM are set by the stage ring.
 //
 // Row stream per tile (the producer runs ahead across passes and tiles):
-//   pass 1 : rows [0, n)             beta' = M'(y - c)     (pass 0 scans the first stage for c)
-//   pass 2 : rows [0, n)             residuals, sigma^2, MOSUM window 0   (re-read: L2 hit)
+//   pass 1 : rows [0, n)             beta_Q = Q^T (y - c) and ||y - c||^2 in ONE sweep
+//                                    (pass 0 scans the first stage for c); sigma follows from
+//                                    RSS = ||y-c||^2 - ||beta_Q||^2 (orthonormal basis Q)
+//   pass 2 : rows [w0, n)            the last ~h history rows again (L2 hit): residuals of
+//                                    MOSUM window 0 into the ring, w0 = 8*floor((n-h+1)/8)
 //   pass 3 : rows [8*floor(n/8), N)  MOSUM recurrence + detect (stages 8-row aligned);
 //            LAG mode: each stage also carries rows t-h (the lagging cursor's input)
+// Measured (profiles/probe): SM-side ingest, DRAM or L2, saturates near 7 TB/s, so re-reading
+// the whole history (342 rows/tile) cost ~1 ms at C2; this stream is 266 rows/tile.
 //
 // MOSUM residual ring (r_{t-h} for the add-one/drop-one recurrence, _kernels.py:31-34):
 //   MODE kRingTmem : in Tensor Memory.  Each thread owns its TMEM lane; ring row q of the
@@ -20,8 +25,12 @@
 //                    >= h) plus 8 mirror rows (L+k == k) so an 8-row window read
 //                    starting anywhere in [0, L) never wraps: one tcgen05.ld.x16 and one
 //                    tcgen05.st.x16 per stage instead of 8 shared loads/stores + index math.
-//   MODE kRingSmem : per-thread shared-memory ring of h rows (small h < 8).
 //   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged row t-h (large h).
+//   (h < 8, where an 8-row batch would read rows it has not written yet, runs the LDG kernel.)
+//
+// Code size matters: the consumer runs one unrolled 8-row body per pass for full stages and
+// a small rolled loop for the (<= 3 per tile) partial stages, so the hot loops stay in the
+// instruction cache; stage/phase and ring positions are tracked incrementally (no div/mod).
 //
 // The monitoring pass runs in the UNSCALED frame: acc = sum of window residuals, crossing
 // test |acc| > b_j * sigma * sqrt(n) (== |MO_j| > b_j), MO = acc / (sigma sqrt n) applied to
@@ -61,6 +70,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
         "r"(parity)
         : "memory");
+}
+// Non-blocking probe: 1 if the phase with this parity has completed (acquire semantics).
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok;
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
@@ -123,6 +144,7 @@ __host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
 
 template <int NP, int MODE>
 __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_tma(const KParams prm) {
+    static_assert(MODE == kRingTmem || MODE == kRingLag, "TMA kernel: TMEM ring or lagging cursor");
     constexpr int SP = Coefs<NP>::SP;
     constexpr int R = kStageRows;
     constexpr int S = kStages;
@@ -130,19 +152,18 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_
     constexpr int ROWF2 = kTile / 2;             // float2 per staged row
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
+    const int n8 = ((n + R - 1) / R) * R;
     const int NA = (N + 3) & ~3;
     unsigned char* s_stage = smem_raw;                                   // [S][SB]
-    float* s_mt = reinterpret_cast<float*>(smem_raw + S * SB);           // [n][SP]
-    float* s_xt = s_mt + n * SP;                                         // [N][SP]
+    float* s_mt = reinterpret_cast<float*>(smem_raw + S * SB);           // [n8][SP] Q^T, rows >= n zero
+    float* s_xt = s_mt + n8 * SP;                                        // [N][SP]  Z^T
     float* s_bd = s_xt + N * SP;                                         // [NA] bound by row t (t >= n)
-    float2* s_ring = reinterpret_cast<float2*>(s_bd + NA);               // [h][kThreads] (kRingSmem)
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(
-        reinterpret_cast<unsigned char*>(s_ring) + (MODE == kRingSmem ? (int64_t)h * kThreads * 8 : 0));
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);
     uint64_t* full = s_bar;          // [S]
     uint64_t* empty = s_bar + S;     // [S]
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * S);
 
-    for (int i = threadIdx.x; i < n * SP; i += kTmaThreads) s_mt[i] = prm.mt[i];
+    for (int i = threadIdx.x; i < n8 * SP; i += kTmaThreads) s_mt[i] = i < n * SP ? prm.mt[i] : 0.f;
     for (int i = threadIdx.x; i < N * SP; i += kTmaThreads) s_xt[i] = prm.xt[i];
     for (int i = threadIdx.x; i < N - n; i += kTmaThreads) s_bd[n + i] = prm.bound[i];
     if (threadIdx.x == 0) {
@@ -160,33 +181,38 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_
     const int64_t n_tiles = prm.n_pixels / kTile;      // host guarantees whole tiles
     const int64_t ld = prm.ld_y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t3 = (n / R) * R;                        // first row of the aligned monitoring stream
+    const int wstart = n - h + 1;                      // first row of MOSUM window 0 (mosum.py:59)
+    const int w0 = (wstart / R) * R;                   // first row of the (aligned) pass-2 stream
+    const int t3 = (n / R) * R;                        // first row of the (aligned) monitoring stream
 
     // =============================== producer ==========================================
     if (warp == kConsumerWarps) {
         if (lane == 0) {
-            uint32_t it = 0;
+            int cur = 0;
+            uint32_t ph = 0;
             for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
                 const float* yt = prm.y + tile * kTile;
+#pragma unroll 1
                 for (int pass = 0; pass < 3; ++pass) {
-                    const int lo = pass == 2 ? t3 : 0, hi = pass == 2 ? N : n;
+                    const int lo = pass == 0 ? 0 : pass == 1 ? w0 : t3;
+                    const int hi = pass == 2 ? N : n;
                     const bool lag = MODE == kRingLag && pass == 2;
                     for (int r0 = lo; r0 < hi; r0 += R) {
                         const int rows = min(R, hi - r0);
-                        const int s = it % S;
-                        mbar_wait(empty + s, ((it / S) & 1) ^ 1);
-                        // lag rows t-h < 0 only occur for skipped rows t < n: clamp their source
-                        int lag_lo = 0;
-                        if (lag) while (lag_lo < rows && r0 + lag_lo - h < 0) ++lag_lo;
-                        mbar_expect_tx(full + s, (uint32_t)((rows + (lag ? rows - lag_lo : 0)) * kRowBytes));
-                        unsigned char* dst = s_stage + s * SB;
+                        mbar_wait(empty + cur, ph ^ 1);
+                        // lag rows t-h < 0 belong to skipped rows t < n: not copied
+                        const int lag_lo = lag ? min(rows, max(0, h - r0)) : 0;
+                        mbar_expect_tx(full + cur, (uint32_t)((rows + (lag ? rows - lag_lo : 0)) * kRowBytes));
+                        unsigned char* dst = s_stage + cur * SB;
+#pragma unroll 1
                         for (int r = 0; r < rows; ++r)
-                            bulk_g2s(dst + r * kRowBytes, yt + (int64_t)(r0 + r) * ld, kRowBytes, full + s);
+                            bulk_g2s(dst + r * kRowBytes, yt + (int64_t)(r0 + r) * ld, kRowBytes, full + cur);
                         if (lag)
+#pragma unroll 1
                             for (int r = lag_lo; r < rows; ++r)
                                 bulk_g2s(dst + (R + r) * kRowBytes, yt + (int64_t)(r0 + r - h) * ld, kRowBytes,
-                                         full + s);
-                        ++it;
+                                         full + cur);
+                        if (++cur == S) { cur = 0; ph ^= 1; }
                     }
                 }
             }
@@ -196,48 +222,63 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_
 
     // =============================== consumers =========================================
     const int tid = threadIdx.x;
-    float2* ring = s_ring + tid;
-    const int wstart = n - h + 1;             // first row of MOSUM window 0 (mosum.py:59)
     const int L = prm.ring_rows;
     const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(warp * 32) << 16) : 0u;
     auto tcol = [&](int row) -> uint32_t { return tbase + (uint32_t)(2 * row); };
-    uint32_t it = 0;
+    // ring row q of time t is t mod L; rows 0..7 are mirrored at L..L+7
+    auto ring_put = [&](int t, float2 v) {
+        const int q = t % L;
+        tmem_st2(tcol(q), v);
+        if (q < R) tmem_st2(tcol(L + q), v);
+    };
+    auto ring_get = [&](int t) -> float2 {
+        uint32_t a, b;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(tcol(t % L))
+                     : "memory");
+        tmem_wait_ld();
+        return f2(__uint_as_float(a), __uint_as_float(b));
+    };
     int cur = 0;
+    uint32_t ph = 0;
+    uint32_t next_ready = 0;     // result of the look-ahead probe of stage `cur`
+    // Waiting on an mbarrier costs a round trip even when the stage has landed; the probe of
+    // the following stage is issued here and consumed at the next acquire.
     auto acquire = [&]() -> const float2* {
-        cur = it % S;
-        mbar_wait(full + cur, (it / S) & 1);
+        if (!next_ready) mbar_wait(full + cur, ph);
+        const int nc = cur + 1 == S ? 0 : cur + 1;
+        next_ready = mbar_test(full + nc, nc == 0 ? ph ^ 1 : ph);
         return reinterpret_cast<const float2*>(s_stage + cur * SB) + tid;
     };
     auto release = [&]() {
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + cur);
-        ++it;
+        if (++cur == S) { cur = 0; ph ^= 1; }
     };
 
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int64_t px0 = tile * kTile + 2 * tid;
         const float* yp = prm.y + px0;
 
-        // ---- pass 1 (+ pass 0 on its first stage) ------------------------------------
+        // ---- pass 1: beta_Q and ||y - c||^2 (+ pass 0 on the first stage) ---------------
         float2 hi[NP], lo[NP], part[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) { hi[i] = lo[i] = part[i] = f2(0.f, 0.f); }
+        float2 qpart = f2(0.f, 0.f);
+        double q0 = 0.0, q1 = 0.0;
         float2 c = f2(0.f, 0.f);
         bool f0 = false, f1 = false;
-        float2 last = f2(0.f, 0.f);
+        float2 last = f2(0.f, 0.f), lastw = f2(0.f, 0.f);
         float2 negc = f2(0.f, 0.f);
         for (int t0 = 0; t0 < n; t0 += R) {
             const float2* st = acquire();
-            const int rows = min(R, n - t0);
             if (t0 == 0) {
                 // pass 0: first finite value (engine.py:316 first = finite.argmax)
-#pragma unroll
-                for (int k = R - 1; k >= 0; --k) {
-                    if (k < rows) {
-                        const float2 v = st[k * ROWF2];
-                        if (finitef(v.x)) { c.x = v.x; f0 = true; }
-                        if (finitef(v.y)) { c.y = v.y; f1 = true; }
-                    }
+                const int rows = min(R, n);
+#pragma unroll 1
+                for (int k = rows - 1; k >= 0; --k) {
+                    const float2 v = st[k * ROWF2];
+                    if (finitef(v.x)) { c.x = v.x; f0 = true; }
+                    if (finitef(v.y)) { c.y = v.y; f1 = true; }
                 }
                 if (!(f0 && f1)) {   // rare: long leading gap or an all-missing pixel
                     for (int t = rows; t < N && !(f0 && f1); ++t) {
@@ -248,171 +289,163 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_
                 }
                 negc = f2(-c.x, -c.y);
             }
-            if (rows == R) {
+            if (t0 + R <= n) {
 #pragma unroll
-                for (int k = 0; k < R; ++k)
-                    axpy_row<NP, SP>(part, fill(st[k * ROWF2], negc, last), s_mt + (t0 + k) * SP);
+                for (int k = 0; k < R; ++k) {
+                    const float2 vc = fill(st[k * ROWF2], negc, last);
+                    axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
+                    qpart = fma2(vc, vc, qpart);
+                }
             } else {
-#pragma unroll
-                for (int k = 0; k < R; ++k)
-                    if (k < rows) axpy_row<NP, SP>(part, fill(st[k * ROWF2], negc, last), s_mt + (t0 + k) * SP);
+#pragma unroll 1
+                for (int k = 0; k < n - t0; ++k) {
+                    const float2 vc = fill(st[k * ROWF2], negc, last);
+                    axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
+                    qpart = fma2(vc, vc, qpart);
+                }
             }
             release();
-            if ((t0 + R) % kComp == 0 || t0 + R >= n) {
+            if (t0 + R == w0) lastw = last;                 // fill state entering pass 2
+            if (((t0 + R) & (kComp - 1)) == 0 || t0 + R >= n) {
 #pragma unroll
                 for (int i = 0; i < NP; ++i) { two_sum(hi[i], lo[i], part[i]); part[i] = f2(0.f, 0.f); }
+                q0 += (double)qpart.x;
+                q1 += (double)qpart.y;
+                qpart = f2(0.f, 0.f);
             }
         }
         const bool valid0 = f0, valid1 = f1;
-        float2 nb[NP];    // -beta'
+        float2 bq[NP], nb[NP];    // beta_Q and -beta_Q
 #pragma unroll
-        for (int i = 0; i < NP; ++i) { const float2 b = add2(hi[i], lo[i]); nb[i] = f2(-b.x, -b.y); }
+        for (int i = 0; i < NP; ++i) { bq[i] = add2(hi[i], lo[i]); nb[i] = f2(-bq[i].x, -bq[i].y); }
 
-        // ---- pass 2: history residuals, sigma^2, MOSUM window 0 ----------------------
-        float2 ss = f2(0.f, 0.f), acc = f2(0.f, 0.f);
-        last = f2(0.f, 0.f);
-        float2 lag_last = f2(0.f, 0.f);          // kRingLag: fill state of the lagging cursor
-        int slot = wstart % h;                   // kRingSmem: slot of row t is t mod h
-        for (int t0 = 0; t0 < n; t0 += R) {
-            const float2* st = acquire();
-            const int rows = min(R, n - t0);
-            if (rows == R && t0 + R < wstart) {
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + (t0 + k) * SP, nb);
-                    ss = fma2(r, r, ss);
-                }
-            } else {
-                float2 rr[R];
-                if (MODE == kRingTmem && rows < R) {
-                    tmem_wait_st();
-                    tmem_ld16(tcol(t0 % L), rr);   // keep ring rows of t >= n (read-modify-write)
-                }
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    if (k < rows) {
-                        const int t = t0 + k;
-                        const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                        ss = fma2(r, r, ss);
-                        rr[k] = r;
-                        if (t >= wstart) {
-                            acc = add2(acc, r);
-                            if (MODE == kRingSmem) {
-                                ring[slot * kThreads] = r;
-                                slot = (slot + 1 == h) ? 0 : slot + 1;
-                            }
-                        }
-                        if (MODE == kRingLag && t == wstart - 1) lag_last = last;
-                    }
-                }
-                if (MODE == kRingTmem) {
-                    const int wb = t0 % L;
-                    tmem_st16(tcol(wb), rr);
-                    if (wb == 0) tmem_st16(tcol(L), rr);
-                }
-            }
-            release();
-        }
-        // the ring slot of r_{n-h} must read as 0: window 0 does not contain it
-        if (MODE == kRingSmem) ring[slot * kThreads] = f2(0.f, 0.f);
-        if (MODE == kRingTmem) {
-            const int z = (n - h) % L;
-            tmem_st2(tcol(z), f2(0.f, 0.f));
-            if (z < R) tmem_st2(tcol(L + z), f2(0.f, 0.f));
-        }
-
-        // sigma (engine.py:363-371) and the zero-sigma contract (engine.py:373-378): the
-        // reference raises when float64 gives sigma == 0 exactly — an identically zero
-        // history (c == 0).  A non-zero constant history has round-off sigma ~1e-17 there
-        // (MO ~1e15): sigma_scale 0 reproduces its decisions (any non-zero window crosses).
+        // sigma (engine.py:363-371) from the one-pass RSS and the zero-sigma contract
+        // (engine.py:373-378): the reference raises when float64 gives sigma == 0 exactly —
+        // an identically zero history (c == 0).  A non-zero constant history has round-off
+        // sigma ~1e-17 there (MO ~1e15): scale 0 reproduces its decisions (any non-zero window
+        // crosses).
+        const float2 ss = rss_onepass<NP>(q0, q1, bq);
         const bool z0 = valid0 && ss.x == 0.f && c.x == 0.f, z1 = valid1 && ss.y == 0.f && c.y == 0.f;
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
         const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);
+
+        // ---- pass 2: residuals of the last history rows -> ring and window 0 --------------
+        float2 acc = f2(0.f, 0.f);
+        last = lastw;
+        float2 lag_last = w0 == wstart ? lastw : f2(0.f, 0.f);   // kRingLag: fill state at wstart-1
+        int wb = MODE == kRingTmem ? w0 % L : 0;
+        for (int t0 = w0; t0 < n; t0 += R) {
+            const float2* st = acquire();
+            if (t0 + R <= n) {
+                float2 rr[R];
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const int t = t0 + k;
+                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+                    rr[k] = r;
+                    if (t >= wstart) acc = add2(acc, r);
+                    if (MODE == kRingLag && t == wstart - 1) lag_last = last;
+                }
+                if (MODE == kRingTmem) {
+                    tmem_st16(tcol(wb), rr);
+                    if (wb == 0) tmem_st16(tcol(L), rr);
+                }
+            } else {
+#pragma unroll 1
+                for (int k = 0; k < n - t0; ++k) {
+                    const int t = t0 + k;
+                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+                    if (MODE == kRingTmem) ring_put(t, r);
+                    if (t >= wstart) acc = add2(acc, r);
+                    if (MODE == kRingLag && t == wstart - 1) lag_last = last;
+                }
+            }
+            release();
+            if (MODE == kRingTmem) { wb += R; if (wb == L) wb = 0; }
+        }
+        if (MODE == kRingTmem) ring_put(n - h, f2(0.f, 0.f));    // r_{n-h} is not in window 0
 
         // ---- pass 3: monitoring period, fused MOSUM + detect (unscaled frame) ----------
         float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f);
         int first0 = 0x7fffffff, first1 = 0x7fffffff;
         float* const mo_out = prm.mosum;
         const float2 inv = inv_scale(sc);
+        auto step = [&](const float2 r, const float2 old, const int t, const float bj) {
+            acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
+            const float2 bs = mul2(sc, f2(bj, bj));   // boundary in the unscaled frame
+            const float a0 = fabsf(acc.x), a1 = fabsf(acc.y);
+            mx.x = fmaxf(mx.x, a0);
+            mx.y = fmaxf(mx.y, a1);
+            const int j1 = t - n + 1;
+            if (a0 > bs.x) first0 = min(first0, j1);  // strict crossing (_kernels.py:47)
+            if (a1 > bs.y) first1 = min(first1, j1);
+            msum = add2(msum, acc);
+            if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)(t - n) * prm.ld_out + px0) = mul2(acc, inv);
+        };
+        wb = MODE == kRingTmem ? t3 % L : 0;
+        int rb = MODE == kRingTmem ? ((t3 - h) % L + L) % L : 0;   // ring row of t0 - h
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
             const float2* lst = st + R * ROWF2;          // lag rows (kRingLag)
-            const bool full_stage = t0 > n && t0 + R <= N;
-            float2 oldv[R], newv[R];
-            if (MODE == kRingTmem) {
-                tmem_wait_st();
-                const int rb = ((t0 - h) % L + L) % L;
-                tmem_ld16(tcol(rb), oldv);
-                if (!full_stage) tmem_ld16(tcol(t0 % L), newv);   // preserve rows t < n
-            }
-            float4 b4[R / 4];
-#pragma unroll
-            for (int q = 0; q < R / 4; ++q) b4[q] = reinterpret_cast<const float4*>(s_bd + t0)[q];
-            auto row = [&](const int k, const bool checked) {
-                const int t = t0 + k;
-                if (checked && (t < n || t >= N)) return;
-                const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                float2 old = f2(0.f, 0.f);
+            if (t0 >= n + (MODE == kRingLag ? 1 : 0) && t0 + R <= N) {
+                float2 oldv[R], newv[R];
                 if (MODE == kRingTmem) {
-                    old = oldv[k];
-                    newv[k] = r;
-                } else if (MODE == kRingSmem) {
-                    old = ring[slot * kThreads];
-                    ring[slot * kThreads] = r;
-                    slot = (slot + 1 == h) ? 0 : slot + 1;
-                } else if (!checked || t > n) {          // r_{t-h}; r_{n-h} is outside window 0
-                    old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
+                    tmem_wait_st();
+                    tmem_ld16(tcol(rb), oldv);
                 }
-                acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
-                const float bj = (k & 3) == 0 ? b4[k >> 2].x : (k & 3) == 1 ? b4[k >> 2].y
-                               : (k & 3) == 2 ? b4[k >> 2].z : b4[k >> 2].w;
-                const float2 bs = mul2(sc, f2(bj, bj));   // boundary in the unscaled frame
-                const float a0 = fabsf(acc.x), a1 = fabsf(acc.y);
-                mx.x = fmaxf(mx.x, a0);
-                mx.y = fmaxf(mx.y, a1);
-                const int j1 = t - n + 1;
-                if (a0 > bs.x) first0 = min(first0, j1);  // strict crossing (_kernels.py:47)
-                if (a1 > bs.y) first1 = min(first1, j1);
-                msum = add2(msum, acc);
-                if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)(t - n) * prm.ld_out + px0) = mul2(acc, inv);
-            };
-            if (full_stage) {
+                float4 b4[R / 4];
 #pragma unroll
-                for (int k = 0; k < R; ++k) row(k, false);
+                for (int q = 0; q < R / 4; ++q) b4[q] = reinterpret_cast<const float4*>(s_bd + t0)[q];
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const int t = t0 + k;
+                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+                    float2 old;
+                    if (MODE == kRingTmem) {
+                        old = oldv[k];
+                        newv[k] = r;
+                    } else {
+                        old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
+                    }
+                    const float4 bq4 = b4[k >> 2];
+                    step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
+                }
+                if (MODE == kRingTmem) {
+                    tmem_st16(tcol(wb), newv);
+                    if (wb == 0) tmem_st16(tcol(L), newv);
+                }
             } else {
-#pragma unroll
-                for (int k = 0; k < R; ++k) row(k, true);
-            }
-            if (MODE == kRingTmem) {
-                const int wb = t0 % L;
-                tmem_st16(tcol(wb), newv);
-                if (wb == 0) tmem_st16(tcol(L), newv);
+                if (MODE == kRingTmem) tmem_wait_st();
+#pragma unroll 1
+                for (int k = 0; k < R; ++k) {
+                    const int t = t0 + k;
+                    if (t < n || t >= N) continue;
+                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+                    float2 old = f2(0.f, 0.f);
+                    if (MODE == kRingTmem) {
+                        old = ring_get(t - h);
+                        ring_put(t, r);
+                    } else if (t > n) {                      // r_{n-h} is outside window 0
+                        old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
+                    }
+                    step(r, old, t, s_bd[t]);
+                }
             }
             release();
+            if (MODE == kRingTmem) {
+                wb += R; if (wb == L) wb = 0;
+                rb += R; if (rb >= L) rb -= L;
+            }
         }
 
         // ---- outputs --------------------------------------------------------------------
-        {
-            const float inv_m = 1.0f / (float)(N - n);
-            *reinterpret_cast<uchar2*>(prm.valid + px0) = make_uchar2(valid0, valid1);
-            *reinterpret_cast<int2*>(prm.first_idx + px0) =
-                make_int2(first0 == 0x7fffffff ? 0 : first0, first1 == 0x7fffffff ? 0 : first1);
-            *reinterpret_cast<float2*>(prm.max_abs + px0) = mul2(mx, inv);
-            if (prm.mo_mean) *reinterpret_cast<float2*>(prm.mo_mean + px0) = mul2(mul2(msum, inv), f2(inv_m, inv_m));
-            if (prm.beta) {
-                // back to the raw basis (bwm.h): b0 = c + b0' - b1' tc/ts, b1 = b1'/ts
-                float2 bo[NP];
-#pragma unroll
-                for (int i = 0; i < NP; ++i) bo[i] = f2(-nb[i].x, -nb[i].y);
-                const float2 b1 = bo[1];
-                bo[0] = add2(c, sub2(bo[0], mul2(b1, f2(prm.tc_ts, prm.tc_ts))));
-                bo[1] = mul2(b1, f2(prm.inv_ts, prm.inv_ts));
-#pragma unroll
-                for (int i = 0; i < NP; ++i)
-                    *reinterpret_cast<float2*>(prm.beta + (int64_t)i * prm.ld_out + px0) =
-                        f2(valid0 ? bo[i].x : 0.f, valid1 ? bo[i].y : 0.f);
-            }
-        }
+        const float inv_m = 1.0f / (float)(N - n);
+        *reinterpret_cast<uchar2*>(prm.valid + px0) = make_uchar2(valid0, valid1);
+        *reinterpret_cast<int2*>(prm.first_idx + px0) =
+            make_int2(first0 == 0x7fffffff ? 0 : first0, first1 == 0x7fffffff ? 0 : first1);
+        *reinterpret_cast<float2*>(prm.max_abs + px0) = mul2(mx, inv);
+        if (prm.mo_mean) *reinterpret_cast<float2*>(prm.mo_mean + px0) = mul2(mul2(msum, inv), f2(inv_m, inv_m));
+        if (prm.beta) store_beta<NP>(prm, px0, c, bq, valid0, valid1, 2);
     }
 
     if (MODE == kRingTmem) {

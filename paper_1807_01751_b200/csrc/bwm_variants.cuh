@@ -9,8 +9,8 @@ using KernelFn = void (*)(const KParams);
 }  // namespace bwm
 
 // Defines bwm::KernelFn bwm_pick_p<NP>(int kind, int mode) in the including TU.
-// mode: bwm::RingMode (kRingSmem / kRingTmem / kRingLag); the LDG kernels have a shared-memory
-// ring (any mode but kRingLag) or the lagging cursor.
+// mode: bwm::RingMode of the TMA kernel (kRingTmem / kRingLag; < 0 = none); the LDG kernels
+// have a shared-memory ring (any mode but kRingLag) or the lagging cursor.
 #define BWM_DEFINE_PICK(NP)                                                                      \
     bwm::KernelFn bwm_pick_p##NP(int kind, int mode) {                                           \
         const bool ring = mode != bwm::kRingLag;                                                 \
@@ -20,8 +20,7 @@ using KernelFn = void (*)(const KParams);
             case bwm::kLdgSafe:                                                                  \
                 return ring ? bwm::monitor_kernel_ldg<NP, true, true> : bwm::monitor_kernel_ldg<NP, true, false>;   \
             default:                                                                             \
-                return mode == bwm::kRingSmem ? bwm::monitor_kernel_tma<NP, bwm::kRingSmem>      \
-                     : mode == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem>      \
+                return mode == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem>      \
                                               : bwm::monitor_kernel_tma<NP, bwm::kRingLag>;      \
         }                                                                                        \
     }

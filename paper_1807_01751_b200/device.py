@@ -1,6 +1,7 @@
 """Device plans: one libbwm plan (constant tables resident on one GPU) per batch geometry.
 
-A plan owns the float32 tables the kernel reads (mapping M', design X', boundary) and is
+A plan owns the float32 tables the kernel reads (orthonormal history basis Q, fitted-value
+rows Z, boundary — libbwm derives Q, Z from the centred design X' in float64) and is
 reused across calls with the same (axis, freq, k, n, h, lambda, device) — the host f64
 setup runs once, like the reference's per-batch design/mapping (engine.py:339-341).
 
@@ -79,7 +80,6 @@ class DevicePlan:
         self.dims = _lib.Dims(self.n_obs, self.n_hist, self.bandwidth, self.n_params)
         dbl = C.POINTER(C.c_double)
         tables = _lib.Tables(
-            basis.mapping.ctypes.data_as(dbl),
             basis.design.ctypes.data_as(dbl),
             np.ascontiguousarray(bound).ctypes.data_as(dbl),
             basis.trend_center,
@@ -112,6 +112,14 @@ class DevicePlan:
                     cls._cache.clear()
                 cls._cache[key] = plan
             return plan
+
+    def info(self) -> dict:
+        """Launch configuration libbwm chose for this plan (bwm_plan_info)."""
+        pi = _lib.PlanInfo()
+        _lib.check(self._lib.bwm_plan_info(self._handle, C.byref(pi)), "bwm_plan_info")
+        d = {name: getattr(pi, name) for name, _ in _lib.PlanInfo._fields_}
+        d["ring_mode"] = {0: "smem", 1: "tmem", 2: "lag"}[d["ring_mode"]]
+        return d
 
     # ------------------------------------------------------------------ device path
     def run_device(self, y, *, keep_mosum: bool = False, beta: bool = False, mean: bool = False,
