@@ -8,6 +8,7 @@
 #include "bwm_variants.cuh"
 
 #include <atomic>
+#include <cudaTypedefs.h>
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
@@ -88,8 +89,37 @@ int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
     const int sp = (p + 3) & ~3;
     const int n8 = ((n + bwm::kStageRows - 1) / bwm::kStageRows) * bwm::kStageRows;
     int64_t fl = (int64_t)n8 * sp + (int64_t)N * sp + ((N + 3) & ~3);
-    int64_t bytes = bwm::kStages * bwm::tma_stage_bytes(mode) + fl * 4;
-    return bytes + 2 * bwm::kStages * 8 + 16;
+    int64_t bytes = bwm::kWarps * bwm::kStages * bwm::tma_stage_bytes(mode) + fl * 4;
+    return bytes + bwm::kWarps * bwm::kStages * 8 + 16;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D map of a time-major float32 block: dim0 = pixels (contiguous), dim1 = dates (stride ld)
+int encode_map(CUtensorMap* map, const float* y, int64_t n_pixels, int n_obs, int64_t ld) {
+    auto fn = encode_fn();
+    if (!fn) return set_err((int)cudaErrorNotSupported, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)n_pixels, (cuuint64_t)n_obs};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)bwm::kWarpPx, (cuuint32_t)bwm::kStageRows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(y), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err((int)cudaErrorInvalidValue, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return BWM_OK;
 }
 
 using bwm::Kind;
@@ -465,6 +495,10 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         const int64_t tiles = (cnt + bwm::kTile - 1) / bwm::kTile;
         const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * plan->blocks_per_sm[kind]);
         const size_t sm = (size_t)(kind == kTma ? plan->smem_tma : plan->smem);
+        if (kind == kTma) {
+            int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y);
+            if (rc) return rc;
+        }
         fn<<<(unsigned)grid, threads_of(kind), sm, st>>>(kp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));

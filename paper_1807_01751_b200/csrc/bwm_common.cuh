@@ -8,6 +8,7 @@
 //     leaves fitted values unchanged in exact arithmetic);
 //   * 16-date FFMA2 block partials are 2Sum-compensated into (hi, lo).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -19,6 +20,7 @@ constexpr int kDepth = 16;            // LDG kernel: prefetch depth == compensat
 constexpr int kComp = 16;             // dates per 2Sum-compensated block partial
 
 struct KParams {
+    CUtensorMap tmap;           // TMA kernel: 2-D map of y (pixels x dates), box 64 px x 8 dates
     const float* y;             // this launch's pixel 0, row stride ld_y (elements)
     int64_t ld_y;
     int64_t n_pixels;

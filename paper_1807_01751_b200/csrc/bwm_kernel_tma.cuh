@@ -1,21 +1,22 @@
-// bwm_kernel_tma.cuh — fused BFAST-monitor kernel, TMA-staged variant (sm_100a, default).
+// bwm_kernel_tma.cuh — fused BFAST-monitor kernel, TMA-pipelined variant (sm_100a, default).
 //
-// CTA = 4 consumer warps (128 threads, one pixel PAIR each -> a 256-pixel tile) + 1
-// producer warp.  The producer streams the tile's rows (1 KB each: 256 float32 pixels of
-// one date) from HBM/L2 into a ring of shared-memory stages with bulk asynchronous copies
-// (cp.async.bulk -> the TMA engine, SASS UBLKCP), signalling an mbarrier per stage with
-// complete_tx; consumers wait on the stage, read their float2 per row (LDS.64,
-// conflict-free) and release the stage with one arrive per warp.  Registers hold only the
-// per-pixel pipeline state; bytes in flight per SM are set by the stage ring.
+// CTA = 4 warps, 128 threads, one pixel PAIR per thread -> a 256-pixel tile; warp w owns the
+// 64-pixel slice [64w, 64w+64) of every tile.  Each warp runs its OWN asynchronous pipeline:
+// lane 0 issues one 2-D tensor TMA per stage (cp.async.bulk.tensor.2d, SASS UTMALDG) that
+// copies a box of 8 dates x 64 pixels (2 KB) of the time-major stack into the warp's stage
+// ring in shared memory and completes an mbarrier with the byte count; the warp waits on
+// it, each lane reads its float2 per date (LDS.64, conflict-free), and after the stage is
+// consumed the same lane re-arms the slot with the stage kStages ahead.  No producer warp,
+// no cross-warp barrier: warps never wait for each other.
 //
-// Row stream per tile (the producer runs ahead across passes and tiles):
+// Row stream per tile (the issue cursor runs kStages ahead across passes and tiles):
 //   pass 1 : rows [0, n)             beta_Q = Q^T (y - c) and ||y - c||^2 in ONE sweep
 //                                    (pass 0 scans the first stage for c); sigma follows from
 //                                    RSS = ||y-c||^2 - ||beta_Q||^2 (orthonormal basis Q)
 //   pass 2 : rows [w0, n)            the last ~h history rows again (L2 hit): residuals of
 //                                    MOSUM window 0 into the ring, w0 = 8*floor((n-h+1)/8)
-//   pass 3 : rows [8*floor(n/8), N)  MOSUM recurrence + detect (stages 8-row aligned);
-//            LAG mode: each stage also carries rows t-h (the lagging cursor's input)
+//   pass 3 : rows [8*floor(n/8), N)  MOSUM recurrence + detect (stages 8-date aligned);
+//            LAG mode: each stage also carries dates t-h (second box; t-h < 0 is OOB zero fill)
 // Measured (profiles/probe): SM-side ingest, DRAM or L2, saturates near 7 TB/s, so re-reading
 // the whole history (342 rows/tile) cost ~1 ms at C2; this stream is 266 rows/tile.
 //
@@ -25,16 +26,13 @@
 //                    >= h) plus 8 mirror rows (L+k == k) so an 8-row window read
 //                    starting anywhere in [0, L) never wraps: one tcgen05.ld.x16 and one
 //                    tcgen05.st.x16 per stage instead of 8 shared loads/stores + index math.
-//   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged row t-h (large h).
+//   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged date t-h (large h).
 //   (h < 8, where an 8-row batch would read rows it has not written yet, runs the LDG kernel.)
-//
-// Code size matters: the consumer runs one unrolled 8-row body per pass for full stages and
-// a small rolled loop for the (<= 3 per tile) partial stages, so the hot loops stay in the
-// instruction cache; stage/phase and ring positions are tracked incrementally (no div/mod).
 //
 // The monitoring pass runs in the UNSCALED frame: acc = sum of window residuals, crossing
 // test |acc| > b_j * sigma * sqrt(n) (== |MO_j| > b_j), MO = acc / (sigma sqrt n) applied to
-// the max/mean at the end.
+// the max/mean at the end.  Full 8-date stages run one unrolled body per pass; the <= 3
+// partial stages per tile run a small rolled loop, keeping the hot code in the I-cache.
 #pragma once
 
 #include "bwm_common.cuh"
@@ -42,10 +40,11 @@
 namespace bwm {
 
 constexpr int kStageRows = 8;                   // dates per stage
-constexpr int kStages = 7;                      // stage ring depth
-constexpr int kRowBytes = kTile * 4;            // one date of one tile
-constexpr int kConsumerWarps = kThreads / 32;
-constexpr int kTmaThreads = kThreads + 32;      // + producer warp
+constexpr int kStages = 5;                      // stage ring depth per warp
+constexpr int kWarpPx = 64;                     // pixels per warp slice (32 lanes x 2)
+constexpr int kBoxBytes = kStageRows * kWarpPx * 4;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTmaThreads = kThreads;
 
 enum RingMode { kRingSmem = 0, kRingTmem = 1, kRingLag = 2 };
 
@@ -58,9 +57,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
@@ -83,11 +79,12 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* b, uint32_t parity) {
         : "memory");
     return ok;
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// 2-D tensor TMA: box (64 px, 8 dates) at (x, y) -> smem, completing `bar` with its bytes.
+__device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -137,40 +134,36 @@ __device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
                  : "memory");
 }
 
-// Shared-memory footprint of the TMA kernel (host mirror in bwm_capi.cu).
+// Shared-memory footprint per warp stage (host mirror in bwm_capi.cu).
 __host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
-    return (int64_t)kStageRows * kRowBytes * (mode == kRingLag ? 2 : 1);
+    return (int64_t)kBoxBytes * (mode == kRingLag ? 2 : 1);
 }
 
 template <int NP, int MODE>
-__global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_tma(const KParams prm) {
+__global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
+    monitor_kernel_tma(const __grid_constant__ KParams prm) {
     static_assert(MODE == kRingTmem || MODE == kRingLag, "TMA kernel: TMEM ring or lagging cursor");
     constexpr int SP = Coefs<NP>::SP;
     constexpr int R = kStageRows;
     constexpr int S = kStages;
     constexpr int64_t SB = tma_stage_bytes(MODE);
-    constexpr int ROWF2 = kTile / 2;             // float2 per staged row
+    constexpr int ROWF2 = kWarpPx / 2;           // float2 per staged row of a warp slice
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
     const int n8 = ((n + R - 1) / R) * R;
     const int NA = (N + 3) & ~3;
-    unsigned char* s_stage = smem_raw;                                   // [S][SB]
-    float* s_mt = reinterpret_cast<float*>(smem_raw + S * SB);           // [n8][SP] Q^T, rows >= n zero
+    unsigned char* s_stage = smem_raw;                                   // [kWarps][S][SB]
+    float* s_mt = reinterpret_cast<float*>(smem_raw + kWarps * S * SB);  // [n8][SP] Q^T, rows >= n zero
     float* s_xt = s_mt + n8 * SP;                                        // [N][SP]  Z^T
     float* s_bd = s_xt + N * SP;                                         // [NA] bound by row t (t >= n)
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);
-    uint64_t* full = s_bar;          // [S]
-    uint64_t* empty = s_bar + S;     // [S]
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * S);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);           // [kWarps][S]
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + kWarps * S);
 
     for (int i = threadIdx.x; i < n8 * SP; i += kTmaThreads) s_mt[i] = i < n * SP ? prm.mt[i] : 0.f;
     for (int i = threadIdx.x; i < N * SP; i += kTmaThreads) s_xt[i] = prm.xt[i];
     for (int i = threadIdx.x; i < N - n; i += kTmaThreads) s_bd[n + i] = prm.bound[i];
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, kConsumerWarps);
-        }
+        for (int s = 0; s < kWarps * S; ++s) mbar_init(s_bar + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (MODE == kRingTmem && threadIdx.x < 32) tmem_alloc(s_tmem, (uint32_t)prm.tmem_cols);
@@ -184,44 +177,35 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_
     const int wstart = n - h + 1;                      // first row of MOSUM window 0 (mosum.py:59)
     const int w0 = (wstart / R) * R;                   // first row of the (aligned) pass-2 stream
     const int t3 = (n / R) * R;                        // first row of the (aligned) monitoring stream
-
-    // =============================== producer ==========================================
-    if (warp == kConsumerWarps) {
-        if (lane == 0) {
-            int cur = 0;
-            uint32_t ph = 0;
-            for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-                const float* yt = prm.y + tile * kTile;
-#pragma unroll 1
-                for (int pass = 0; pass < 3; ++pass) {
-                    const int lo = pass == 0 ? 0 : pass == 1 ? w0 : t3;
-                    const int hi = pass == 2 ? N : n;
-                    const bool lag = MODE == kRingLag && pass == 2;
-                    for (int r0 = lo; r0 < hi; r0 += R) {
-                        const int rows = min(R, hi - r0);
-                        mbar_wait(empty + cur, ph ^ 1);
-                        // lag rows t-h < 0 belong to skipped rows t < n: not copied
-                        const int lag_lo = lag ? min(rows, max(0, h - r0)) : 0;
-                        mbar_expect_tx(full + cur, (uint32_t)((rows + (lag ? rows - lag_lo : 0)) * kRowBytes));
-                        unsigned char* dst = s_stage + cur * SB;
-#pragma unroll 1
-                        for (int r = 0; r < rows; ++r)
-                            bulk_g2s(dst + r * kRowBytes, yt + (int64_t)(r0 + r) * ld, kRowBytes, full + cur);
-                        if (lag)
-#pragma unroll 1
-                            for (int r = lag_lo; r < rows; ++r)
-                                bulk_g2s(dst + (R + r) * kRowBytes, yt + (int64_t)(r0 + r - h) * ld, kRowBytes,
-                                         full + cur);
-                        if (++cur == S) { cur = 0; ph ^= 1; }
-                    }
-                }
-            }
-        }
-        return;
-    }
-
-    // =============================== consumers =========================================
     const int tid = threadIdx.x;
+    unsigned char* my_stage = s_stage + warp * S * SB;
+    uint64_t* full = s_bar + warp * S;
+
+    // ---- this warp's TMA issue cursor: (tile, pass, first date), kStages ahead -----------
+    int64_t itile = blockIdx.x;
+    int ipass = 0, ir0 = 0, islot = 0;
+    auto issue = [&]() {
+        if (itile >= n_tiles) return;
+        if (lane == 0) {
+            const bool lag = MODE == kRingLag && ipass == 2;
+            uint64_t* bar = full + islot;
+            unsigned char* dst = my_stage + islot * SB;
+            const int x = (int)(itile * kTile) + warp * kWarpPx;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // slot was read by the generic proxy
+            mbar_expect_tx(bar, (uint32_t)(lag ? 2 * kBoxBytes : kBoxBytes));
+            tma_box(dst, &prm.tmap, x, ir0, bar);
+            if (lag) tma_box(dst + kBoxBytes, &prm.tmap, x, ir0 - h, bar);   // dates t-h (< 0: zero fill)
+        }
+        ir0 += R;
+        if (ir0 >= (ipass == 2 ? N : n)) {
+            if (++ipass == 3) { ipass = 0; itile += gridDim.x; }
+            ir0 = ipass == 0 ? 0 : ipass == 1 ? w0 : t3;
+        }
+        if (++islot == S) islot = 0;
+    };
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap)) : "memory");
+    for (int s = 0; s < S; ++s) issue();
+
     const int L = prm.ring_rows;
     const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(warp * 32) << 16) : 0u;
     auto tcol = [&](int row) -> uint32_t { return tbase + (uint32_t)(2 * row); };
@@ -247,11 +231,11 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_
         if (!next_ready) mbar_wait(full + cur, ph);
         const int nc = cur + 1 == S ? 0 : cur + 1;
         next_ready = mbar_test(full + nc, nc == 0 ? ph ^ 1 : ph);
-        return reinterpret_cast<const float2*>(s_stage + cur * SB) + tid;
+        return reinterpret_cast<const float2*>(my_stage + cur * SB) + lane;
     };
     auto release = [&]() {
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty + cur);
+        issue();                                     // re-arm this slot kStages ahead
         if (++cur == S) { cur = 0; ph ^= 1; }
     };
 
@@ -386,7 +370,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_
         int rb = MODE == kRingTmem ? ((t3 - h) % L + L) % L : 0;   // ring row of t0 - h
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
-            const float2* lst = st + R * ROWF2;          // lag rows (kRingLag)
+            const float2* lst = st + kBoxBytes / 8;      // lag dates (kRingLag): second box
             if (t0 >= n + (MODE == kRingLag ? 1 : 0) && t0 + R <= N) {
                 float2 oldv[R], newv[R];
                 if (MODE == kRingTmem) {
@@ -451,7 +435,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 3 : 2) monitor_kernel_
     if (MODE == kRingTmem) {
         tmem_wait_st();
         tmem_fence_before();
-        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");   // consumer warps only
+        __syncthreads();
         tmem_fence_after();
         if (warp == 0) tmem_dealloc(*s_tmem, (uint32_t)prm.tmem_cols);
     }

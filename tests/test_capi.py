@@ -84,12 +84,12 @@ def test_null_arguments_rejected_without_device():
 
 
 def test_sass_contains_blackwell_async_copy_and_tensor_memory():
-    """The default kernel is built for sm_100a and uses the TMA engine (UBLKCP) and Tensor
+    """The default kernel is built for sm_100a and uses tensor TMA (UTMALDG) and Tensor
     Memory (LDTM/STTM) — evidence checked on the shipped .so, not on a cached build."""
     from paper_1807_01751_b200 import _lib
 
     out = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", str(_lib.LIB_PATH)], capture_output=True,
                                        text=True).stdout
-    for mnemonic in ("UBLKCP", "LDTM", "STTM", "FFMA2", "SYNCS"):
+    for mnemonic in ("UTMALDG", "LDTM", "STTM", "FFMA2", "SYNCS"):
         assert mnemonic in out, mnemonic
