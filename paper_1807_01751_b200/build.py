@@ -51,7 +51,17 @@ def _compile(src: Path, force: bool) -> tuple[Path, str]:
     return obj, res.stderr
 
 
-def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None, defines=(), out: Path | None = None,
+          obj_dir: Path | None = None) -> Path:
+    """Compile and link libbwm.so.  `defines` (e.g. ["BWM_STAGE_ROWS=16"]) and `out`/`obj_dir`
+    build an experimental variant next to the default library (A/B runs via BWM_LIB)."""
+    global OBJ, LIB
+    if defines:
+        NVCC_FLAGS.extend(f"-D{d}" for d in defines)
+    if out is not None:
+        LIB = Path(out)
+    if obj_dir is not None:
+        OBJ = Path(obj_dir)
     OBJ.mkdir(parents=True, exist_ok=True)
     sources = sorted(CSRC.glob("*.cu"))
     jobs = jobs or min(len(sources), os.cpu_count() or 4)
@@ -74,5 +84,15 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
 
 
 if __name__ == "__main__":
-    path = build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(path)
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("-D", action="append", default=[], help="extra preprocessor define")
+    ap.add_argument("--out", default=None, help="library path (default: in-tree libbwm.so)")
+    args = ap.parse_args()
+    obj = None
+    if args.out:
+        obj = Path(args.out).resolve().parent / ("obj_" + Path(args.out).stem)
+    print(build(force=args.force, verbose=args.v, defines=args.D, out=args.out, obj_dir=obj))

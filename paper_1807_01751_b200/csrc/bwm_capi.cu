@@ -71,14 +71,15 @@ struct TmaRing {
     int mode, rows, cols;
 };
 TmaRing tma_ring_for(int h) {
-    const int L = ((h + 7) / 8) * 8;
-    const int need = 2 * (L + 8);
-    if (h >= 8 && need <= 256) {
+    constexpr int R = bwm::kStageRows;
+    const int L = ((h + R - 1) / R) * R;
+    const int need = 2 * (L + R);
+    if (h >= R && need <= 256) {
         int cols = 32;
         while (cols < need) cols *= 2;
         return {bwm::kRingTmem, L, cols};
     }
-    return {h < 8 ? -1 : (int)bwm::kRingLag, 0, 0};   // -1: no TMA variant (LDG kernel)
+    return {h < R ? -1 : (int)bwm::kRingLag, 0, 0};   // -1: no TMA variant (LDG kernel)
 }
 
 // shared memory of the TMA kernel: stages + tables (mapping padded to 8-row stages, bound

@@ -22,25 +22,33 @@
 //
 // MOSUM residual ring (r_{t-h} for the add-one/drop-one recurrence, _kernels.py:31-34):
 //   MODE kRingTmem : in Tensor Memory.  Each thread owns its TMEM lane; ring row q of the
-//                    pixel pair occupies columns 2q, 2q+1.  L = ring rows (multiple of 8,
-//                    >= h) plus 8 mirror rows (L+k == k) so an 8-row window read
-//                    starting anywhere in [0, L) never wraps: one tcgen05.ld.x16 and one
-//                    tcgen05.st.x16 per stage instead of 8 shared loads/stores + index math.
+//                    pixel pair occupies columns 2q, 2q+1.  L = ring rows (multiple of the
+//                    stage height R, >= h) plus R mirror rows (L+k == k) so an R-row window
+//                    read starting anywhere in [0, L) never wraps: R/8 tcgen05.ld.x16 and
+//                    tcgen05.st.x16 per stage instead of R shared loads/stores + index math.
 //   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged date t-h (large h).
-//   (h < 8, where an 8-row batch would read rows it has not written yet, runs the LDG kernel.)
+//   (h < R, where an R-row batch would read rows it has not written yet, runs the LDG kernel.)
 //
 // The monitoring pass runs in the UNSCALED frame: acc = sum of window residuals, crossing
 // test |acc| > b_j * sigma * sqrt(n) (== |MO_j| > b_j), MO = acc / (sigma sqrt n) applied to
-// the max/mean at the end.  Full 8-date stages run one unrolled body per pass; the <= 3
-// partial stages per tile run a small rolled loop, keeping the hot code in the I-cache.
+// the max/mean at the end.  Each pass is ONE unrolled R-date body; the partial stages at pass
+// boundaries are handled by warp-uniform row predicates (and read-modify-write of ring rows),
+// so the hot code stays small enough for the instruction cache.
 #pragma once
 
 #include "bwm_common.cuh"
 
 namespace bwm {
 
-constexpr int kStageRows = 8;                   // dates per stage
-constexpr int kStages = 5;                      // stage ring depth per warp
+#ifndef BWM_STAGE_ROWS
+#define BWM_STAGE_ROWS 8
+#endif
+#ifndef BWM_STAGES
+#define BWM_STAGES 5
+#endif
+constexpr int kStageRows = BWM_STAGE_ROWS;      // dates per stage (multiple of 8)
+constexpr int kStages = BWM_STAGES;             // stage ring depth per warp
+static_assert(kStageRows == 8 || kStageRows == 16, "stage height: 8 or 16 dates (compensation blocks are 16)");
 constexpr int kWarpPx = 64;                     // pixels per warp slice (32 lanes x 2)
 constexpr int kBoxBytes = kStageRows * kWarpPx * 4;
 constexpr int kWarps = kThreads / 32;
@@ -79,12 +87,31 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* b, uint32_t parity) {
         : "memory");
     return ok;
 }
-// 2-D tensor TMA: box (64 px, 8 dates) at (x, y) -> smem, completing `bar` with its bytes.
-__device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+// 2-D tensor TMA: box (64 px, R dates) at (x, y) -> smem, completing `bar` with its bytes.
+// Executed by the whole warp; one elected lane arms the barrier and issues the copy (no
+// divergent branch, operands are warp-uniform).
+__device__ __forceinline__ void tma_box_elect(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                              uint32_t bytes) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n\t"
+        "}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void tma_box2_elect(uint32_t dst, const CUtensorMap* map, int x, int y, int y2,
+                                               uint32_t bar, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%5], %6;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%2, {%3, %4}], [%5];\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%1], [%2, {%3, %7}], [%5];\n\t"
+        "}" ::"r"(dst),
+        "r"(dst + (uint32_t)(kStageRows * kWarpPx * 4)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
+        "r"(bar), "r"(bytes), "r"(y2)
         : "memory");
 }
 
@@ -178,49 +205,58 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
     const int w0 = (wstart / R) * R;                   // first row of the (aligned) pass-2 stream
     const int t3 = (n / R) * R;                        // first row of the (aligned) monitoring stream
     const int tid = threadIdx.x;
-    unsigned char* my_stage = s_stage + warp * S * SB;
-    uint64_t* full = s_bar + warp * S;
+    const int wu = __shfl_sync(0xffffffffu, warp, 0);              // warp index, known warp-uniform
+    unsigned char* my_stage = s_stage + wu * S * SB;
+    uint64_t* full = s_bar + wu * S;
+    const uint32_t stage_u32 = smem_u32(my_stage), bar_u32 = smem_u32(full);
 
-    // ---- this warp's TMA issue cursor: (tile, pass, first date), kStages ahead -----------
+    // ---- this warp's TMA issue cursor, kStages ahead of consumption ----------------------
+    // The per-tile stage schedule (first date of each stage; pass 3 flagged) is a table, so
+    // re-arming a slot is a lookup.  The slot being re-armed was read by this warp through
+    // the generic proxy; __syncwarp() in release() orders those reads before lane 0 issues
+    // the copy (the same release->acquire ordering an mbarrier handshake gives a producer).
+    const int st1 = (n + R - 1) / R, st2 = (n - w0 + R - 1) / R;
+    const int tile_stages = st1 + st2 + (N - t3 + R - 1) / R;
     int64_t itile = blockIdx.x;
-    int ipass = 0, ir0 = 0, islot = 0;
+    int istage = 0, islot = 0;
     auto issue = [&]() {
         if (itile >= n_tiles) return;
-        if (lane == 0) {
-            const bool lag = MODE == kRingLag && ipass == 2;
-            uint64_t* bar = full + islot;
-            unsigned char* dst = my_stage + islot * SB;
-            const int x = (int)(itile * kTile) + warp * kWarpPx;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // slot was read by the generic proxy
-            mbar_expect_tx(bar, (uint32_t)(lag ? 2 * kBoxBytes : kBoxBytes));
-            tma_box(dst, &prm.tmap, x, ir0, bar);
-            if (lag) tma_box(dst + kBoxBytes, &prm.tmap, x, ir0 - h, bar);   // dates t-h (< 0: zero fill)
-        }
-        ir0 += R;
-        if (ir0 >= (ipass == 2 ? N : n)) {
-            if (++ipass == 3) { ipass = 0; itile += gridDim.x; }
-            ir0 = ipass == 0 ? 0 : ipass == 1 ? w0 : t3;
-        }
+        const int r0 = istage < st1 ? istage * R : istage < st1 + st2 ? w0 + (istage - st1) * R
+                                                                        : t3 + (istage - st1 - st2) * R;
+        const int x = (int)(itile * kTile) + wu * kWarpPx;
+        const uint32_t dst = stage_u32 + (uint32_t)(islot * SB), bar = bar_u32 + (uint32_t)(islot * 8);
+        if (MODE == kRingLag && istage >= st1 + st2)
+            tma_box2_elect(dst, &prm.tmap, x, r0, r0 - h, bar, 2 * kBoxBytes);   // + dates t-h (<0: zero fill)
+        else
+            tma_box_elect(dst, &prm.tmap, x, r0, bar, kBoxBytes);
+        if (++istage == tile_stages) { istage = 0; itile += gridDim.x; }
         if (++islot == S) islot = 0;
     };
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap)) : "memory");
     for (int s = 0; s < S; ++s) issue();
 
     const int L = prm.ring_rows;
-    const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(warp * 32) << 16) : 0u;
+    const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(wu * 32) << 16) : 0u;
     auto tcol = [&](int row) -> uint32_t { return tbase + (uint32_t)(2 * row); };
-    // ring row q of time t is t mod L; rows 0..7 are mirrored at L..L+7
+    // ring row q of time t is t mod L; rows 0..R-1 are mirrored at L..L+R-1
     auto ring_put = [&](int t, float2 v) {
         const int q = t % L;
         tmem_st2(tcol(q), v);
         if (q < R) tmem_st2(tcol(L + q), v);
     };
-    auto ring_get = [&](int t) -> float2 {
-        uint32_t a, b;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(tcol(t % L))
-                     : "memory");
-        tmem_wait_ld();
-        return f2(__uint_as_float(a), __uint_as_float(b));
+    // R consecutive ring rows starting at row q0 (q0 + R <= L + R: never wraps)
+    auto ring_load = [&](int q0, float2 (&v)[R]) {
+        tmem_wait_st();
+#pragma unroll
+        for (int c8 = 0; c8 < R / 8; ++c8) tmem_ld16(tcol(q0 + 8 * c8), *reinterpret_cast<float2(*)[8]>(&v[8 * c8]));
+    };
+    auto ring_store = [&](int q0, const float2 (&v)[R]) {   // q0 multiple of R: mirror when q0 == 0
+#pragma unroll
+        for (int c8 = 0; c8 < R / 8; ++c8) {
+            const float2(&part8)[8] = *reinterpret_cast<const float2(*)[8]>(&v[8 * c8]);
+            tmem_st16(tcol(q0 + 8 * c8), part8);
+            if (q0 == 0) tmem_st16(tcol(L + 8 * c8), part8);
+        }
     };
     int cur = 0;
     uint32_t ph = 0;
@@ -273,20 +309,13 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
                 }
                 negc = f2(-c.x, -c.y);
             }
-            if (t0 + R <= n) {
+            // rows >= n of the last stage: zero mapping rows (exact no-ops) and no q update; the
+            // fill state they leave behind is reset before pass 2
 #pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const float2 vc = fill(st[k * ROWF2], negc, last);
-                    axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
-                    qpart = fma2(vc, vc, qpart);
-                }
-            } else {
-#pragma unroll 1
-                for (int k = 0; k < n - t0; ++k) {
-                    const float2 vc = fill(st[k * ROWF2], negc, last);
-                    axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
-                    qpart = fma2(vc, vc, qpart);
-                }
+            for (int k = 0; k < R; ++k) {
+                const float2 vc = fill(st[k * ROWF2], negc, last);
+                axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
+                if (t0 + k < n) qpart = fma2(vc, vc, qpart);
             }
             release();
             if (t0 + R == w0) lastw = last;                 // fill state entering pass 2
@@ -320,30 +349,19 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
         int wb = MODE == kRingTmem ? w0 % L : 0;
         for (int t0 = w0; t0 < n; t0 += R) {
             const float2* st = acquire();
-            if (t0 + R <= n) {
-                float2 rr[R];
+            float2 rr[R];
+            if (MODE == kRingTmem && t0 + R > n) ring_load(wb, rr);   // keep ring rows of dates >= n
 #pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const int t = t0 + k;
+            for (int k = 0; k < R; ++k) {
+                const int t = t0 + k;
+                if (t < n) {                                   // warp-uniform
                     const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
                     rr[k] = r;
                     if (t >= wstart) acc = add2(acc, r);
                     if (MODE == kRingLag && t == wstart - 1) lag_last = last;
                 }
-                if (MODE == kRingTmem) {
-                    tmem_st16(tcol(wb), rr);
-                    if (wb == 0) tmem_st16(tcol(L), rr);
-                }
-            } else {
-#pragma unroll 1
-                for (int k = 0; k < n - t0; ++k) {
-                    const int t = t0 + k;
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                    if (MODE == kRingTmem) ring_put(t, r);
-                    if (t >= wstart) acc = add2(acc, r);
-                    if (MODE == kRingLag && t == wstart - 1) lag_last = last;
-                }
             }
+            if (MODE == kRingTmem) ring_store(wb, rr);
             release();
             if (MODE == kRingTmem) { wb += R; if (wb == L) wb = 0; }
         }
@@ -371,50 +389,35 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
             const float2* lst = st + kBoxBytes / 8;      // lag dates (kRingLag): second box
-            if (t0 >= n + (MODE == kRingLag ? 1 : 0) && t0 + R <= N) {
-                float2 oldv[R], newv[R];
-                if (MODE == kRingTmem) {
-                    tmem_wait_st();
-                    tmem_ld16(tcol(rb), oldv);
-                }
-                float4 b4[R / 4];
+            float2 oldv[R], newv[R];
+            if (MODE == kRingTmem) {
+                ring_load(rb, oldv);
+                if (t0 < n) ring_load(wb, newv);         // first stage: keep the history rows
+            }
+            float4 b4[R / 4];
 #pragma unroll
-                for (int q = 0; q < R / 4; ++q) b4[q] = reinterpret_cast<const float4*>(s_bd + t0)[q];
+            for (int q = 0; q < R / 4; ++q) b4[q] = reinterpret_cast<const float4*>(s_bd + t0)[q];
 #pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const int t = t0 + k;
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+            for (int k = 0; k < R; ++k) {
+                const int t = t0 + k;
+                // dates < n were filled in pass 2 already: re-filling them from the state at n-1
+                // ends in the same state (idempotent), so only the MOSUM step is skipped
+                const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+                if (t >= n && t < N) {                   // warp-uniform
                     float2 old;
                     if (MODE == kRingTmem) {
                         old = oldv[k];
                         newv[k] = r;
                     } else {
-                        old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
+                        old = f2(0.f, 0.f);
+                        if (t > n)                       // r_{n-h} is outside window 0
+                            old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
                     }
                     const float4 bq4 = b4[k >> 2];
                     step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
                 }
-                if (MODE == kRingTmem) {
-                    tmem_st16(tcol(wb), newv);
-                    if (wb == 0) tmem_st16(tcol(L), newv);
-                }
-            } else {
-                if (MODE == kRingTmem) tmem_wait_st();
-#pragma unroll 1
-                for (int k = 0; k < R; ++k) {
-                    const int t = t0 + k;
-                    if (t < n || t >= N) continue;
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                    float2 old = f2(0.f, 0.f);
-                    if (MODE == kRingTmem) {
-                        old = ring_get(t - h);
-                        ring_put(t, r);
-                    } else if (t > n) {                      // r_{n-h} is outside window 0
-                        old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
-                    }
-                    step(r, old, t, s_bd[t]);
-                }
             }
+            if (MODE == kRingTmem) ring_store(wb, newv);
             release();
             if (MODE == kRingTmem) {
                 wb += R; if (wb == L) wb = 0;
