@@ -232,6 +232,7 @@ def run_ours(args):
     with ClockSampler(local) as clocks:
         barrier(world)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("bench_timed")
         t_begin = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_begin.record(stream)
@@ -240,6 +241,7 @@ def run_ours(args):
             plan.run_device(y, out=res, check_zero=False)
             ends[i].record(stream)
         t_end.record(stream)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         barrier(world)
     launches = _lib.launch_count() - launches0

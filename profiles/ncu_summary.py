@@ -51,9 +51,11 @@ def main():
             print(f"    {h.replace('smsp__average_warp_latency_issue_stalled_', ''):50s} {v:8.3f}")
         if len(sys.argv) > 2:
             alg = float(sys.argv[2])
-            rd = float(r[hdr.index("dram__bytes_read.sum")].replace(",", ""))
-            wr = float(r[hdr.index("dram__bytes_write.sum")].replace(",", ""))
-            print(f"  dram traffic / algorithmic bytes = {(rd + wr) / alg:.3f}")
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+            def val(k):
+                return float(r[hdr.index(k)].replace(",", "")) * scale[units[hdr.index(k)]]
+            tot = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+            print(f"  dram traffic per launch = {tot:.6e} B; algorithmic = {alg:.6e} B; ratio = {tot / alg:.4f}")
 
 
 if __name__ == "__main__":

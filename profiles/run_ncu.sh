@@ -6,7 +6,7 @@ set -e
 TAG=${1:-r01}
 WL=${2:-C2}
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum --clock-control none -c 12 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "bench_timed/" -c 400 --csv \
     --log-file gpurun_out/launches_${TAG}_${WL}.csv \
     python bench.py --workload $WL --steps 4 --warmup 2 --no-e2e --no-cpu > gpurun_out/launches_${TAG}_${WL}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:monitor_kernel -s 3 -c 1 \
