@@ -9,6 +9,7 @@
 //   * 16-date FFMA2 block partials are 2Sum-compensated into (hi, lo).
 #pragma once
 #include <cuda.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -17,7 +18,7 @@ namespace bwm {
 constexpr int kThreads = 128;
 constexpr int kTile = 2 * kThreads;   // pixels per CTA tile
 constexpr int kDepth = 16;            // LDG kernel: prefetch depth == compensation block (dates)
-constexpr int kComp = 16;             // dates per 2Sum-compensated block partial
+constexpr int kComp = 32;             // dates per 2Sum-compensated block partial (emulated 1e-5)
 
 struct KParams {
     CUtensorMap tmap;           // TMA kernel: 2-D map of y (pixels x dates), box 64 px x 8 dates

@@ -104,11 +104,10 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         double q0 = 0.0, q1 = 0.0;           // ||y - c||^2 (16-date float32 partials, float64 sum)
         float2 last = f2(0.f, 0.f);
         const float* pf = yp + (int64_t)D * ld;   // refill target of the row being consumed
-        for (int t0 = 0; t0 < n; t0 += D) {
-            float2 part[NP];
+        float2 part[NP], qpart = f2(0.f, 0.f);
 #pragma unroll
-            for (int i = 0; i < NP; ++i) part[i] = f2(0.f, 0.f);
-            float2 qpart = f2(0.f, 0.f);
+        for (int i = 0; i < NP; ++i) part[i] = f2(0.f, 0.f);
+        for (int t0 = 0; t0 < n; t0 += D) {
             if (t0 + 2 * D <= n) {
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
@@ -136,10 +135,13 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                     }
                 }
             }
+            if ((t0 + D) % kComp == 0 || t0 + D >= n) {   // same blocks as the TMA kernel
 #pragma unroll
-            for (int i = 0; i < NP; ++i) two_sum(hi[i], lo[i], part[i]);
-            q0 += (double)qpart.x;
-            q1 += (double)qpart.y;
+                for (int i = 0; i < NP; ++i) { two_sum(hi[i], lo[i], part[i]); part[i] = f2(0.f, 0.f); }
+                q0 += (double)qpart.x;
+                q1 += (double)qpart.y;
+                qpart = f2(0.f, 0.f);
+            }
         }
         float2 bq[NP], nb[NP];    // beta_Q and -beta_Q
 #pragma unroll

@@ -311,12 +311,18 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
             }
             // rows >= n of the last stage: zero mapping rows (exact no-ops) and no q update; the
             // fill state they leave behind is reset before pass 2
+            auto body1 = [&](auto full_tag) {
+                constexpr bool FULL = decltype(full_tag)::value;
+                const float* mrow = s_mt + t0 * SP;
 #pragma unroll
-            for (int k = 0; k < R; ++k) {
-                const float2 vc = fill(st[k * ROWF2], negc, last);
-                axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
-                if (t0 + k < n) qpart = fma2(vc, vc, qpart);
-            }
+                for (int k = 0; k < R; ++k) {
+                    const float2 vc = fill(st[k * ROWF2], negc, last);
+                    axpy_row<NP, SP>(part, vc, mrow + k * SP);
+                    if (FULL || t0 + k < n) qpart = fma2(vc, vc, qpart);
+                }
+            };
+            if (t0 + R <= n) body1(std::true_type{});
+            else body1(std::false_type{});
             release();
             if (t0 + R == w0) lastw = last;                 // fill state entering pass 2
             if (((t0 + R) & (kComp - 1)) == 0 || t0 + R >= n) {
@@ -351,16 +357,22 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
             const float2* st = acquire();
             float2 rr[R];
             if (MODE == kRingTmem && t0 + R > n) ring_load(wb, rr);   // keep ring rows of dates >= n
+            auto body2 = [&](auto full_tag) {
+                constexpr bool FULL = decltype(full_tag)::value;
+                const float* xrow = s_xt + t0 * SP;
 #pragma unroll
-            for (int k = 0; k < R; ++k) {
-                const int t = t0 + k;
-                if (t < n) {                                   // warp-uniform
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                    rr[k] = r;
-                    if (t >= wstart) acc = add2(acc, r);
-                    if (MODE == kRingLag && t == wstart - 1) lag_last = last;
+                for (int k = 0; k < R; ++k) {
+                    const int t = t0 + k;
+                    if (FULL || t < n) {                           // warp-uniform
+                        const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), xrow + k * SP, nb);
+                        rr[k] = r;
+                        if (t >= wstart) acc = add2(acc, r);
+                        if (MODE == kRingLag && t == wstart - 1) lag_last = last;
+                    }
                 }
-            }
+            };
+            if (t0 + R <= n) body2(std::true_type{});
+            else body2(std::false_type{});
             if (MODE == kRingTmem) ring_store(wb, rr);
             release();
             if (MODE == kRingTmem) { wb += R; if (wb == L) wb = 0; }
@@ -397,26 +409,32 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
             float4 b4[R / 4];
 #pragma unroll
             for (int q = 0; q < R / 4; ++q) b4[q] = reinterpret_cast<const float4*>(s_bd + t0)[q];
+            auto body3 = [&](auto full_tag) {
+                constexpr bool FULL = decltype(full_tag)::value;
+                const float* xrow = s_xt + t0 * SP;
 #pragma unroll
-            for (int k = 0; k < R; ++k) {
-                const int t = t0 + k;
-                // dates < n were filled in pass 2 already: re-filling them from the state at n-1
-                // ends in the same state (idempotent), so only the MOSUM step is skipped
-                const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                if (t >= n && t < N) {                   // warp-uniform
-                    float2 old;
-                    if (MODE == kRingTmem) {
-                        old = oldv[k];
-                        newv[k] = r;
-                    } else {
-                        old = f2(0.f, 0.f);
-                        if (t > n)                       // r_{n-h} is outside window 0
-                            old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
+                for (int k = 0; k < R; ++k) {
+                    const int t = t0 + k;
+                    // dates < n were filled in pass 2 already: re-filling them from the state at
+                    // n-1 ends in the same state (idempotent), so only the MOSUM step is skipped
+                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), xrow + k * SP, nb);
+                    if (FULL || (t >= n && t < N)) {             // warp-uniform
+                        float2 old;
+                        if (MODE == kRingTmem) {
+                            old = oldv[k];
+                            newv[k] = r;
+                        } else {
+                            old = f2(0.f, 0.f);
+                            if (FULL || t > n)                   // r_{n-h} is outside window 0
+                                old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), xrow + (k - h) * SP, nb);
+                        }
+                        const float4 bq4 = b4[k >> 2];
+                        step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
                     }
-                    const float4 bq4 = b4[k >> 2];
-                    step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
                 }
-            }
+            };
+            if (t0 >= n + (MODE == kRingLag ? 1 : 0) && t0 + R <= N) body3(std::true_type{});
+            else body3(std::false_type{});
             if (MODE == kRingTmem) ring_store(wb, newv);
             release();
             if (MODE == kRingTmem) {
