@@ -244,6 +244,17 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
         tmem_st2(tcol(q), v);
         if (q < R) tmem_st2(tcol(L + q), v);
     };
+    // one ring row (columns 2q, 2q+1); q < L + R
+    auto ring_put_row = [&](int q, float2 v) {
+        tmem_st2(tcol(q), v);
+        if (q < R) tmem_st2(tcol(L + q), v);                  // keep the mirror consistent
+    };
+    auto ring_get_row = [&](int q) -> float2 {
+        uint32_t a, b;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(tcol(q)) : "memory");
+        tmem_wait_ld();
+        return f2(__uint_as_float(a), __uint_as_float(b));
+    };
     // R consecutive ring rows starting at row q0 (q0 + R <= L + R: never wraps)
     auto ring_load = [&](int q0, float2 (&v)[R]) {
         tmem_wait_st();
@@ -311,18 +322,22 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
             }
             // rows >= n of the last stage: zero mapping rows (exact no-ops) and no q update; the
             // fill state they leave behind is reset before pass 2
-            auto body1 = [&](auto full_tag) {
-                constexpr bool FULL = decltype(full_tag)::value;
+            if (t0 + R <= n) {
                 const float* mrow = s_mt + t0 * SP;
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const float2 vc = fill(st[k * ROWF2], negc, last);
                     axpy_row<NP, SP>(part, vc, mrow + k * SP);
-                    if (FULL || t0 + k < n) qpart = fma2(vc, vc, qpart);
+                    qpart = fma2(vc, vc, qpart);
                 }
-            };
-            if (t0 + R <= n) body1(std::true_type{});
-            else body1(std::false_type{});
+            } else {                                            // last stage: dates [t0, n) only
+#pragma unroll 1
+                for (int k = 0; k < n - t0; ++k) {
+                    const float2 vc = fill(st[k * ROWF2], negc, last);
+                    axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
+                    qpart = fma2(vc, vc, qpart);
+                }
+            }
             release();
             if (t0 + R == w0) lastw = last;                 // fill state entering pass 2
             if (((t0 + R) & (kComp - 1)) == 0 || t0 + R >= n) {
@@ -355,25 +370,29 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
         int wb = MODE == kRingTmem ? w0 % L : 0;
         for (int t0 = w0; t0 < n; t0 += R) {
             const float2* st = acquire();
-            float2 rr[R];
-            if (MODE == kRingTmem && t0 + R > n) ring_load(wb, rr);   // keep ring rows of dates >= n
-            auto body2 = [&](auto full_tag) {
-                constexpr bool FULL = decltype(full_tag)::value;
+            if (t0 + R <= n) {
+                float2 rr[R];
                 const float* xrow = s_xt + t0 * SP;
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const int t = t0 + k;
-                    if (FULL || t < n) {                           // warp-uniform
-                        const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), xrow + k * SP, nb);
-                        rr[k] = r;
-                        if (t >= wstart) acc = add2(acc, r);
-                        if (MODE == kRingLag && t == wstart - 1) lag_last = last;
-                    }
+                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), xrow + k * SP, nb);
+                    rr[k] = r;
+                    if (t >= wstart) acc = add2(acc, r);
+                    if (MODE == kRingLag && t == wstart - 1) lag_last = last;
                 }
-            };
-            if (t0 + R <= n) body2(std::true_type{});
-            else body2(std::false_type{});
-            if (MODE == kRingTmem) ring_store(wb, rr);
+                if (MODE == kRingTmem) ring_store(wb, rr);
+            } else {                                            // last stage: dates [t0, n) only
+                if (MODE == kRingTmem) tmem_wait_st();
+#pragma unroll 1
+                for (int k = 0; k < n - t0; ++k) {
+                    const int t = t0 + k;
+                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+                    if (MODE == kRingTmem) ring_put_row(wb + k, r);
+                    if (t >= wstart) acc = add2(acc, r);
+                    if (MODE == kRingLag && t == wstart - 1) lag_last = last;
+                }
+            }
             release();
             if (MODE == kRingTmem) { wb += R; if (wb == L) wb = 0; }
         }
@@ -401,41 +420,46 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? 4 : 2)
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
             const float2* lst = st + kBoxBytes / 8;      // lag dates (kRingLag): second box
-            float2 oldv[R], newv[R];
-            if (MODE == kRingTmem) {
-                ring_load(rb, oldv);
-                if (t0 < n) ring_load(wb, newv);         // first stage: keep the history rows
-            }
-            float4 b4[R / 4];
+            if (t0 >= n + (MODE == kRingLag ? 1 : 0) && t0 + R <= N) {
+                float2 oldv[R], newv[R];
+                if (MODE == kRingTmem) ring_load(rb, oldv);
+                float4 b4[R / 4];
 #pragma unroll
-            for (int q = 0; q < R / 4; ++q) b4[q] = reinterpret_cast<const float4*>(s_bd + t0)[q];
-            auto body3 = [&](auto full_tag) {
-                constexpr bool FULL = decltype(full_tag)::value;
+                for (int q = 0; q < R / 4; ++q) b4[q] = reinterpret_cast<const float4*>(s_bd + t0)[q];
                 const float* xrow = s_xt + t0 * SP;
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const int t = t0 + k;
-                    // dates < n were filled in pass 2 already: re-filling them from the state at
-                    // n-1 ends in the same state (idempotent), so only the MOSUM step is skipped
                     const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), xrow + k * SP, nb);
-                    if (FULL || (t >= n && t < N)) {             // warp-uniform
-                        float2 old;
-                        if (MODE == kRingTmem) {
-                            old = oldv[k];
-                            newv[k] = r;
-                        } else {
-                            old = f2(0.f, 0.f);
-                            if (FULL || t > n)                   // r_{n-h} is outside window 0
-                                old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), xrow + (k - h) * SP, nb);
-                        }
-                        const float4 bq4 = b4[k >> 2];
-                        step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
+                    float2 old;
+                    if (MODE == kRingTmem) {
+                        old = oldv[k];
+                        newv[k] = r;
+                    } else {
+                        old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), xrow + (k - h) * SP, nb);
                     }
+                    const float4 bq4 = b4[k >> 2];
+                    step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
                 }
-            };
-            if (t0 >= n + (MODE == kRingLag ? 1 : 0) && t0 + R <= N) body3(std::true_type{});
-            else body3(std::false_type{});
-            if (MODE == kRingTmem) ring_store(wb, newv);
+                if (MODE == kRingTmem) ring_store(wb, newv);
+            } else {
+                // boundary stage: dates [max(t0, n), min(t0 + R, N)), one at a time
+                if (MODE == kRingTmem) tmem_wait_st();
+                const int k0 = max(0, n - t0), k1 = min(R, N - t0);
+#pragma unroll 1
+                for (int k = k0; k < k1; ++k) {
+                    const int t = t0 + k;
+                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
+                    float2 old = f2(0.f, 0.f);
+                    if (MODE == kRingTmem) {
+                        old = ring_get_row(rb + k);           // rb + k < L + R: mirror rows cover the wrap
+                        ring_put_row(wb + k, r);
+                    } else if (t > n) {                        // r_{n-h} is outside window 0
+                        old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
+                    }
+                    step(r, old, t, s_bd[t]);
+                }
+            }
             release();
             if (MODE == kRingTmem) {
                 wb += R; if (wb == L) wb = 0;
