@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BWM_ABI_VERSION 2
+#define BWM_ABI_VERSION 3
 
 /* error codes (negative); positive returns are cudaError_t values */
 #define BWM_OK 0
@@ -83,6 +83,11 @@ typedef struct bwm_outputs {
        to INT64_MAX (device pointer for bwm_monitor, host pointer for bwm_monitor_host).
        Mirrors ZeroResidualError (engine.py:373-378). */
     int64_t* zero_sigma_pixel;
+    /* Optional maps in the reference BreakMap dtypes (engine.py:147-150, 297-299), produced on
+       the device so the host does no conversion pass: NULL to skip. */
+    int64_t* first_break;    /* [P]  n + first_idx, 0 = no break (1-based observation number)     */
+    double* max_abs_f64;     /* [P]  max_abs widened to float64                                    */
+    uint8_t* detected;       /* [P]  first_break > 0                                               */
 } bwm_outputs;
 
 typedef struct bwm_plan bwm_plan;
@@ -104,10 +109,12 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
 
 /*
  * End-to-end call with HOST buffers (the reference-facing path: a numpy stack in,
- * numpy maps out).  Pixels are processed in column chunks; the H2D copy of chunk
- * i+1 overlaps the kernel of chunk i and the D2H of chunk i-1 on separate streams.
- * y_host may be pageable or pinned (pinned is faster).  Blocks until done.
- * Outputs are host pointers with the same layout as bwm_outputs.
+ * numpy maps out).  When the stack fits in device memory it is copied as one contiguous
+ * block (full PCIe rate) and monitored by one launch; otherwise pixels are processed in
+ * column chunks with the H2D of chunk i+1 overlapping the kernel of chunk i and the D2H
+ * of chunk i-1 on separate streams.  y_host may be pageable or pinned (pinned is faster).
+ * Blocks until done.  Outputs are host pointers with the same layout as bwm_outputs;
+ * first_idx / max_abs may be NULL here when first_break / max_abs_f64 are given.
  */
 int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t n_pixels,
                      int64_t pixel_offset, const bwm_outputs* out_host);

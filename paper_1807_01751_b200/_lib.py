@@ -51,6 +51,9 @@ class Outputs(C.Structure):
         ("mosum", C.c_void_p),
         ("ld_out", C.c_int64),
         ("zero_sigma_pixel", C.c_void_p),
+        ("first_break", C.c_void_p),
+        ("max_abs_f64", C.c_void_p),
+        ("detected", C.c_void_p),
     ]
 
 
@@ -98,7 +101,7 @@ def load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.bwm_abi_version() != 2:
+    if lib.bwm_abi_version() != 3:
         raise RuntimeError("libbwm ABI version mismatch; rebuild the library")
     _lib = lib
     return lib

@@ -29,6 +29,11 @@ BWM_DECLARE_PICK(14)
 BWM_DECLARE_PICK(16)
 BWM_DECLARE_PICK(18)
 
+namespace bwm {
+cudaError_t launch_finalize(const int32_t* first_idx, const float* max_abs, int64_t P, int n, int64_t* first_break,
+                            double* mx64, uint8_t* detected, cudaStream_t s);
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -171,7 +176,11 @@ struct HostPipe {
     float* d_beta[2] = {nullptr, nullptr};
     float* d_mean[2] = {nullptr, nullptr};
     float* d_mosum[2] = {nullptr, nullptr};
+    int64_t* d_fb[2] = {nullptr, nullptr};     // first_break (int64)
+    double* d_mx64[2] = {nullptr, nullptr};    // max_abs (float64)
+    uint8_t* d_det[2] = {nullptr, nullptr};    // detected
     int64_t* d_zero = nullptr;         // [2]
+    size_t bytes = 0;                  // device memory held by the pipeline
     cudaStream_t s_h2d[2] = {nullptr, nullptr};
     cudaStream_t s_k[2] = {nullptr, nullptr};
     cudaEvent_t ev_in[2], ev_k0[2], ev_k1[2], ev_free[2];
@@ -392,6 +401,9 @@ static void pipe_free(HostPipe& hp) {
         cudaFree(hp.d_beta[b]);
         cudaFree(hp.d_mean[b]);
         cudaFree(hp.d_mosum[b]);
+        cudaFree(hp.d_fb[b]);
+        cudaFree(hp.d_mx64[b]);
+        cudaFree(hp.d_det[b]);
         if (hp.s_h2d[b]) cudaStreamDestroy(hp.s_h2d[b]);
         if (hp.s_k[b]) cudaStreamDestroy(hp.s_k[b]);
         if (hp.events) {
@@ -505,27 +517,54 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
         ++launched;
     }
+    if (out->first_break || out->max_abs_f64 || out->detected) {
+        cudaError_t e = bwm::launch_finalize(out->first_idx, out->max_abs, n_pixels, d.n_hist, out->first_break,
+                                             out->max_abs_f64, out->detected, st);
+        if (e != cudaSuccess) return set_err((int)e, "finalize launch failed: %s", cudaGetErrorString(e));
+        ++launched;
+    }
     g_launches.fetch_add(launched);
     return BWM_OK;
 }
 
-static int pipe_ensure(bwm_plan* plan, int64_t chunk, bool beta, bool mean, bool mosum) {
+struct PipeNeeds {
+    bool beta, mean, mosum, fb, mx64, det;
+};
+
+static size_t pipe_bytes(const bwm_dims& d, int64_t chunk, int nbuf, const PipeNeeds& w) {
+    size_t per = (size_t)d.n_obs * chunk * 4 + (size_t)chunk * (1 + 4 + 4);
+    if (w.beta) per += (size_t)d.n_params * chunk * 4;
+    if (w.mean) per += (size_t)chunk * 4;
+    if (w.mosum) per += (size_t)(d.n_obs - d.n_hist) * chunk * 4;
+    if (w.fb) per += (size_t)chunk * 8;
+    if (w.mx64) per += (size_t)chunk * 8;
+    if (w.det) per += (size_t)chunk;
+    return per * nbuf;
+}
+
+static int pipe_ensure(bwm_plan* plan, int64_t chunk, int nbuf, const PipeNeeds& w) {
     HostPipe& hp = plan->pipe;
     const bwm_dims& d = plan->dims;
-    const bool need_realloc = hp.chunk != chunk || (beta && !hp.d_beta[0]) || (mean && !hp.d_mean[0]) ||
-                              (mosum && !hp.d_mosum[0]);
-    if (!need_realloc) return BWM_OK;
+    const bool ok = hp.chunk == chunk && hp.nbuf == nbuf && (!w.beta || hp.d_beta[0]) && (!w.mean || hp.d_mean[0]) &&
+                    (!w.mosum || hp.d_mosum[0]) && (!w.fb || hp.d_fb[0]) && (!w.mx64 || hp.d_mx64[0]) &&
+                    (!w.det || hp.d_det[0]);
+    if (ok) return BWM_OK;
     pipe_free(hp);
     hp.chunk = chunk;
-    hp.nbuf = 2;
+    hp.nbuf = nbuf;
     for (int b = 0; b < 2; ++b) {
-        BWM_CUDA(cudaMalloc(&hp.d_y[b], (size_t)d.n_obs * chunk * 4));
-        BWM_CUDA(cudaMalloc(&hp.d_valid[b], (size_t)chunk));
-        BWM_CUDA(cudaMalloc(&hp.d_first[b], (size_t)chunk * 4));
-        BWM_CUDA(cudaMalloc(&hp.d_max[b], (size_t)chunk * 4));
-        if (beta) BWM_CUDA(cudaMalloc(&hp.d_beta[b], (size_t)d.n_params * chunk * 4));
-        if (mean) BWM_CUDA(cudaMalloc(&hp.d_mean[b], (size_t)chunk * 4));
-        if (mosum) BWM_CUDA(cudaMalloc(&hp.d_mosum[b], (size_t)(d.n_obs - d.n_hist) * chunk * 4));
+        if (b < nbuf) {
+            BWM_CUDA(cudaMalloc(&hp.d_y[b], (size_t)d.n_obs * chunk * 4));
+            BWM_CUDA(cudaMalloc(&hp.d_valid[b], (size_t)chunk));
+            BWM_CUDA(cudaMalloc(&hp.d_first[b], (size_t)chunk * 4));
+            BWM_CUDA(cudaMalloc(&hp.d_max[b], (size_t)chunk * 4));
+            if (w.beta) BWM_CUDA(cudaMalloc(&hp.d_beta[b], (size_t)d.n_params * chunk * 4));
+            if (w.mean) BWM_CUDA(cudaMalloc(&hp.d_mean[b], (size_t)chunk * 4));
+            if (w.mosum) BWM_CUDA(cudaMalloc(&hp.d_mosum[b], (size_t)(d.n_obs - d.n_hist) * chunk * 4));
+            if (w.fb) BWM_CUDA(cudaMalloc(&hp.d_fb[b], (size_t)chunk * 8));
+            if (w.mx64) BWM_CUDA(cudaMalloc(&hp.d_mx64[b], (size_t)chunk * 8));
+            if (w.det) BWM_CUDA(cudaMalloc(&hp.d_det[b], (size_t)chunk));
+        }
         BWM_CUDA(cudaStreamCreateWithFlags(&hp.s_h2d[b], cudaStreamNonBlocking));
         BWM_CUDA(cudaStreamCreateWithFlags(&hp.s_k[b], cudaStreamNonBlocking));
         BWM_CUDA(cudaEventCreateWithFlags(&hp.ev_in[b], cudaEventDisableTiming));
@@ -535,14 +574,17 @@ static int pipe_ensure(bwm_plan* plan, int64_t chunk, bool beta, bool mean, bool
     }
     hp.events = true;
     BWM_CUDA(cudaMalloc(&hp.d_zero, 2 * sizeof(int64_t)));
+    hp.bytes = pipe_bytes(d, chunk, nbuf, w);
     return BWM_OK;
 }
 
 int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t n_pixels,
                      int64_t pixel_offset, const bwm_outputs* out) {
     if (!plan) return set_err(BWM_E_NULL, "plan is NULL");
-    if (!y_host || !out || !out->valid || !out->first_idx || !out->max_abs || !out->zero_sigma_pixel)
-        return set_err(BWM_E_NULL, "y and outputs valid/first_idx/max_abs/zero_sigma_pixel are required");
+    if (!y_host || !out || !out->valid || !out->zero_sigma_pixel || !(out->first_idx || out->first_break) ||
+        !(out->max_abs || out->max_abs_f64))
+        return set_err(BWM_E_NULL,
+                       "y, valid, zero_sigma_pixel, first_idx|first_break and max_abs|max_abs_f64 are required");
     if (n_pixels < 1) return set_err(BWM_E_DIMS, "stack needs at least one pixel");
     if (ld_y < n_pixels) return set_err(BWM_E_DIMS, "ld_y < n_pixels");
     if ((out->beta || out->mosum) && out->ld_out < n_pixels) return set_err(BWM_E_DIMS, "ld_out < n_pixels");
@@ -552,12 +594,26 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
     BWM_CUDA(cudaSetDevice(plan->device));
     const bwm_dims& d = plan->dims;
     const int N = d.n_obs, M = d.n_obs - d.n_hist, p = d.n_params;
+    const PipeNeeds need{out->beta != nullptr, out->mo_mean != nullptr, out->mosum != nullptr,
+                         out->first_break != nullptr, out->max_abs_f64 != nullptr, out->detected != nullptr};
 
-    // chunk: ~512 MB of y per buffer, multiple of the CTA tile
-    int64_t chunk = (512ll << 20) / (4ll * N);
-    chunk = std::max<int64_t>(bwm::kTile, (chunk / bwm::kTile) * bwm::kTile);
-    if (chunk >= n_pixels) chunk = ((n_pixels + bwm::kTile - 1) / bwm::kTile) * bwm::kTile;
-    int rc = pipe_ensure(plan, chunk, out->beta != nullptr, out->mo_mean != nullptr, out->mosum != nullptr);
+    // Whole-stack mode when it fits (one contiguous H2D at full PCIe rate, one launch);
+    // otherwise ~512 MB column chunks, double-buffered.
+    size_t free_b = 0, total_b = 0;
+    BWM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t avail = free_b + plan->pipe.bytes;
+    const int64_t whole = ((n_pixels + bwm::kTile - 1) / bwm::kTile) * bwm::kTile;
+    int64_t chunk;
+    int nbuf;
+    if (pipe_bytes(d, whole, 1, need) + (512ull << 20) <= avail) {
+        chunk = whole;
+        nbuf = 1;
+    } else {
+        chunk = (512ll << 20) / (4ll * N);
+        chunk = std::max<int64_t>(bwm::kTile, (chunk / bwm::kTile) * bwm::kTile);
+        nbuf = 2;
+    }
+    int rc = pipe_ensure(plan, chunk, nbuf, need);
     if (rc) return rc;
     HostPipe& hp = plan->pipe;
 
@@ -575,16 +631,34 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
     std::vector<cudaEvent_t> kev((size_t)(2 * n_chunks), nullptr);   // per-chunk kernel timing
     for (auto& ev : kev) BWM_CUDA(cudaEventCreate(&ev));
     for (int64_t c = 0; c < n_chunks; ++c) {
-        const int b = (int)(c & 1);
+        const int b = nbuf == 1 ? 0 : (int)(c & 1);
         const int64_t p0 = c * chunk;
         const int64_t w = std::min(chunk, n_pixels - p0);
-        // buffer b is free once chunk c-2 finished its D2H
-        if (c >= 2) BWM_CUDA(cudaStreamWaitEvent(hp.s_h2d[b], hp.ev_free[b], 0));
-        BWM_CUDA(cudaMemcpy2DAsync(hp.d_y[b], (size_t)w * 4, y_host + p0, (size_t)ld_y * 4,
-                                   (size_t)w * 4, (size_t)N, cudaMemcpyHostToDevice, hp.s_h2d[b]));
+        cudaStream_t sh = hp.s_h2d[b], s = hp.s_k[b];
+        // buffer b is free once chunk c-nbuf finished its D2H
+        if (c >= nbuf) BWM_CUDA(cudaStreamWaitEvent(sh, hp.ev_free[b], 0));
+        if (ld_y == w) {
+            // contiguous block: split in two halves on both copy streams (one engine each)
+            const size_t total = (size_t)w * 4 * N, half = (total / 2) & ~(size_t)255;
+            BWM_CUDA(cudaMemcpyAsync(hp.d_y[b], y_host + p0, half, cudaMemcpyHostToDevice, sh));
+            if (nbuf == 1) {
+                BWM_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hp.d_y[b]) + half,
+                                         reinterpret_cast<const char*>(y_host + p0) + half, total - half,
+                                         cudaMemcpyHostToDevice, hp.s_h2d[1]));
+                BWM_CUDA(cudaEventRecord(hp.ev_in[1], hp.s_h2d[1]));
+                BWM_CUDA(cudaStreamWaitEvent(s, hp.ev_in[1], 0));
+            } else {
+                BWM_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hp.d_y[b]) + half,
+                                         reinterpret_cast<const char*>(y_host + p0) + half, total - half,
+                                         cudaMemcpyHostToDevice, sh));
+            }
+        } else {
+            BWM_CUDA(cudaMemcpy2DAsync(hp.d_y[b], (size_t)w * 4, y_host + p0, (size_t)ld_y * 4, (size_t)w * 4,
+                                       (size_t)N, cudaMemcpyHostToDevice, sh));
+        }
         h2d += (int64_t)w * 4 * N;
-        BWM_CUDA(cudaEventRecord(hp.ev_in[b], hp.s_h2d[b]));
-        BWM_CUDA(cudaStreamWaitEvent(hp.s_k[b], hp.ev_in[b], 0));
+        BWM_CUDA(cudaEventRecord(hp.ev_in[b], sh));
+        BWM_CUDA(cudaStreamWaitEvent(s, hp.ev_in[b], 0));
         bwm_outputs o{};
         o.valid = hp.d_valid[b];
         o.first_idx = hp.d_first[b];
@@ -594,19 +668,25 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
         o.mosum = out->mosum ? hp.d_mosum[b] : nullptr;
         o.ld_out = w;
         o.zero_sigma_pixel = hp.d_zero + b;
-        BWM_CUDA(cudaEventRecord(kev[2 * c], hp.s_k[b]));
-        rc = bwm_monitor(plan, hp.d_y[b], w, w, pixel_offset + p0, &o, hp.s_k[b]);
+        o.first_break = out->first_break ? hp.d_fb[b] : nullptr;
+        o.max_abs_f64 = out->max_abs_f64 ? hp.d_mx64[b] : nullptr;
+        o.detected = out->detected ? hp.d_det[b] : nullptr;
+        BWM_CUDA(cudaEventRecord(kev[2 * c], s));
+        rc = bwm_monitor(plan, hp.d_y[b], w, w, pixel_offset + p0, &o, s);
         if (rc) return rc;
-        BWM_CUDA(cudaEventRecord(kev[2 * c + 1], hp.s_k[b]));
-        cudaStream_t s = hp.s_k[b];
-        BWM_CUDA(cudaMemcpyAsync(out->valid + p0, hp.d_valid[b], (size_t)w, cudaMemcpyDeviceToHost, s));
-        BWM_CUDA(cudaMemcpyAsync(out->first_idx + p0, hp.d_first[b], (size_t)w * 4, cudaMemcpyDeviceToHost, s));
-        BWM_CUDA(cudaMemcpyAsync(out->max_abs + p0, hp.d_max[b], (size_t)w * 4, cudaMemcpyDeviceToHost, s));
-        d2h += w * 9;
-        if (out->mo_mean) {
-            BWM_CUDA(cudaMemcpyAsync(out->mo_mean + p0, hp.d_mean[b], (size_t)w * 4, cudaMemcpyDeviceToHost, s));
-            d2h += w * 4;
-        }
+        BWM_CUDA(cudaEventRecord(kev[2 * c + 1], s));
+        auto d2h_copy = [&](void* dst, const void* src, size_t bytes) -> int {
+            BWM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+            d2h += (int64_t)bytes;
+            return BWM_OK;
+        };
+        if ((rc = d2h_copy(out->valid + p0, hp.d_valid[b], (size_t)w))) return rc;
+        if (out->first_idx && (rc = d2h_copy(out->first_idx + p0, hp.d_first[b], (size_t)w * 4))) return rc;
+        if (out->max_abs && (rc = d2h_copy(out->max_abs + p0, hp.d_max[b], (size_t)w * 4))) return rc;
+        if (out->first_break && (rc = d2h_copy(out->first_break + p0, hp.d_fb[b], (size_t)w * 8))) return rc;
+        if (out->max_abs_f64 && (rc = d2h_copy(out->max_abs_f64 + p0, hp.d_mx64[b], (size_t)w * 8))) return rc;
+        if (out->detected && (rc = d2h_copy(out->detected + p0, hp.d_det[b], (size_t)w))) return rc;
+        if (out->mo_mean && (rc = d2h_copy(out->mo_mean + p0, hp.d_mean[b], (size_t)w * 4))) return rc;
         if (out->beta) {
             BWM_CUDA(cudaMemcpy2DAsync(out->beta + p0, (size_t)out->ld_out * 4, hp.d_beta[b], (size_t)w * 4,
                                        (size_t)w * 4, (size_t)p, cudaMemcpyDeviceToHost, s));

@@ -38,10 +38,32 @@ class DeviceResult:
     mo_mean: object = None   # float32 [P]
     mosum: object = None     # float32 [N-n, P]
     zero_sigma: Optional[int] = None   # lowest global pixel with sigma == 0, if any
+    first_break: object = None         # int64 [P]: n + first_idx, 0 = none (reference dtype)
+    max_abs_f64: object = None         # float64 [P]
+    detected: object = None            # uint8 [P]
     kernel_ms: float = 0.0
     total_ms: float = 0.0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+
+
+_TORCH_DTYPES = {}
+
+
+def _pinned(shape, dtype):
+    """numpy array backed by page-locked host memory (torch's caching host allocator, so
+    steady-state calls reuse blocks): the D2H of the result maps runs at PCIe rate instead of
+    staging through pageable memory.  Falls back to plain numpy without a CUDA runtime."""
+    try:
+        import torch
+
+        if not _TORCH_DTYPES:
+            _TORCH_DTYPES.update({np.dtype(np.uint8): torch.uint8, np.dtype(np.int32): torch.int32,
+                                  np.dtype(np.int64): torch.int64, np.dtype(np.float32): torch.float32,
+                                  np.dtype(np.float64): torch.float64})
+        return torch.empty(shape, dtype=_TORCH_DTYPES[np.dtype(dtype)], pin_memory=True).numpy()
+    except (RuntimeError, ImportError):
+        return np.empty(shape, dtype=dtype)
 
 
 def _axis_key(axis: TimeAxis) -> str:
@@ -124,7 +146,7 @@ class DevicePlan:
     # ------------------------------------------------------------------ device path
     def run_device(self, y, *, keep_mosum: bool = False, beta: bool = False, mean: bool = False,
                    pixel_offset: int = 0, stream=None, out: Optional[DeviceResult] = None,
-                   check_zero: bool = True) -> DeviceResult:
+                   check_zero: bool = True, ref_dtypes: bool = False) -> DeviceResult:
         """Monitor a device-resident stack y: float32 CUDA tensor (N, P), unit pixel stride."""
         import torch
 
@@ -148,13 +170,16 @@ class DevicePlan:
                 mosum=torch.empty((self.n_obs - self.n_hist, P), dtype=torch.float32, device=dev)
                 if keep_mosum else None,
             )
+            if ref_dtypes:
+                out.first_break = torch.empty(P, dtype=torch.int64, device=dev)
+                out.max_abs_f64 = torch.empty(P, dtype=torch.float64, device=dev)
+                out.detected = torch.empty(P, dtype=torch.uint8, device=dev)
         zero = torch.full((1,), _lib.INT64_MAX, dtype=torch.int64, device=dev)
+        dp = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
         o = _lib.Outputs(
             out.valid.data_ptr(), out.first_idx.data_ptr(), out.max_abs.data_ptr(),
-            out.beta.data_ptr() if out.beta is not None else None,
-            out.mo_mean.data_ptr() if out.mo_mean is not None else None,
-            out.mosum.data_ptr() if out.mosum is not None else None,
-            P, zero.data_ptr(),
+            dp(out.beta), dp(out.mo_mean), dp(out.mosum), P, zero.data_ptr(),
+            dp(out.first_break), dp(out.max_abs_f64), dp(out.detected),
         )
         with torch.cuda.device(dev):
             s = stream if stream is not None else torch.cuda.current_stream(dev)
@@ -169,8 +194,13 @@ class DevicePlan:
 
     # ------------------------------------------------------------------ host path
     def run_host(self, y: np.ndarray, *, keep_mosum: bool = False, beta: bool = False, mean: bool = False,
-                 pixel_offset: int = 0) -> DeviceResult:
-        """Monitor a host stack y: float32 (N, P) C-order numpy array (pinned is fastest)."""
+                 pixel_offset: int = 0, ref_dtypes: bool = False) -> DeviceResult:
+        """Monitor a host stack y: float32 (N, P) C-order numpy array (pinned is fastest).
+
+        ref_dtypes: return first_break (int64), max_abs_f64 (float64) and detected (uint8)
+        computed on the device — the reference BreakMap dtypes, no host conversion pass —
+        instead of the raw first_idx / max_abs maps.
+        """
         y = np.asarray(y)
         if y.dtype != np.float32 or y.ndim != 2 or y.strides[1] != 4:
             raise ValueError("run_host needs a float32 (N, P) array with unit pixel stride")
@@ -178,17 +208,22 @@ class DevicePlan:
             raise ValueError(f"expected y of shape ({self.n_obs}, P), got {y.shape}")
         P = int(y.shape[1])
         out = DeviceResult(
-            valid=np.empty(P, dtype=np.uint8),
-            first_idx=np.empty(P, dtype=np.int32),
-            max_abs=np.empty(P, dtype=np.float32),
-            beta=np.empty((self.n_params, P), dtype=np.float32) if beta else None,
-            mo_mean=np.empty(P, dtype=np.float32) if mean else None,
-            mosum=np.empty((self.n_obs - self.n_hist, P), dtype=np.float32) if keep_mosum else None,
+            valid=_pinned(P, np.uint8),
+            first_idx=None if ref_dtypes else _pinned(P, np.int32),
+            max_abs=None if ref_dtypes else _pinned(P, np.float32),
+            beta=_pinned((self.n_params, P), np.float32) if beta else None,
+            mo_mean=_pinned(P, np.float32) if mean else None,
+            mosum=_pinned((self.n_obs - self.n_hist, P), np.float32) if keep_mosum else None,
         )
+        if ref_dtypes:
+            out.first_break = _pinned(P, np.int64)
+            out.max_abs_f64 = _pinned(P, np.float64)
+            out.detected = _pinned(P, np.uint8)
         zero = np.array([_lib.INT64_MAX], dtype=np.int64)
         ptr = lambda a: a.ctypes.data if a is not None else None  # noqa: E731
         o = _lib.Outputs(ptr(out.valid), ptr(out.first_idx), ptr(out.max_abs), ptr(out.beta),
-                         ptr(out.mo_mean), ptr(out.mosum), P, zero.ctypes.data)
+                         ptr(out.mo_mean), ptr(out.mosum), P, zero.ctypes.data,
+                         ptr(out.first_break), ptr(out.max_abs_f64), ptr(out.detected))
         t0 = time.perf_counter()
         _lib.check(self._lib.bwm_monitor_host(self._handle, y.ctypes.data, y.strides[0] // 4, P,
                                               int(pixel_offset), C.byref(o)), "bwm_monitor_host")

@@ -260,36 +260,33 @@ def _run(stack, config, threads, block_size, keep_mosum, return_beta, return_mea
         import torch
 
         mark = clock()
-        res = plan.run_device(stack.data, keep_mosum=keep_mosum, beta=return_beta, mean=return_mean)
+        res = plan.run_device(stack.data, keep_mosum=keep_mosum, beta=return_beta, mean=return_mean,
+                              ref_dtypes=True)
         torch.cuda.synchronize(plan.torch_device)
         t_kernel = clock() - mark
         mark = clock()
-        res = DeviceResult(
-            valid=res.valid.cpu().numpy(), first_idx=res.first_idx.cpu().numpy(),
-            max_abs=res.max_abs.cpu().numpy(),
-            beta=None if res.beta is None else res.beta.cpu().numpy(),
-            mo_mean=None if res.mo_mean is None else res.mo_mean.cpu().numpy(),
-            mosum=None if res.mosum is None else res.mosum.cpu().numpy(),
-            zero_sigma=res.zero_sigma,
-        )
+        host = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
+        res = DeviceResult(valid=host(res.valid), first_idx=None, max_abs=None, beta=host(res.beta),
+                           mo_mean=host(res.mo_mean), mosum=host(res.mosum), zero_sigma=res.zero_sigma,
+                           first_break=host(res.first_break), max_abs_f64=host(res.max_abs_f64),
+                           detected=host(res.detected))
         t_ingest, t_d2h = 0.0, clock() - mark
     else:
-        res = plan.run_host(stack.data, keep_mosum=keep_mosum, beta=return_beta, mean=return_mean)
+        res = plan.run_host(stack.data, keep_mosum=keep_mosum, beta=return_beta, mean=return_mean,
+                            ref_dtypes=True)
         t_kernel = res.kernel_ms * 1e-3
         t_ingest = max(0.0, (res.total_ms - res.kernel_ms) * 1e-3)
         t_d2h = 0.0
     if res.zero_sigma is not None:
         raise ZeroResidualError(f"pixel {res.zero_sigma} fits its history exactly (sigma = 0)")
 
+    # the maps arrive in the reference dtypes (engine.py:147-150, 297-299): no conversion pass
     mark = clock()
-    first_idx = res.first_idx.astype(np.int64)
-    detected = first_idx > 0
-    first_break = np.where(detected, n + first_idx, 0)
     break_map = BreakMap(
-        detected=detected,
-        first_break=first_break,
-        max_abs_mo=res.max_abs.astype(np.float64),
-        valid=res.valid.astype(bool),
+        detected=res.detected.view(bool),
+        first_break=res.first_break,
+        max_abs_mo=res.max_abs_f64,
+        valid=res.valid.view(bool),
         config=config,
         crit_value=crit,
         mosum=None if res.mosum is None else res.mosum.astype(np.float64),

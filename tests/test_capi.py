@@ -42,7 +42,7 @@ def test_abi_version_and_error_string():
     from paper_1807_01751_b200 import _lib
 
     lib = _lib.load()
-    assert lib.bwm_abi_version() == 2
+    assert lib.bwm_abi_version() == 3
     assert isinstance(lib.bwm_last_error(), bytes)
 
 
