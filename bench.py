@@ -125,9 +125,15 @@ def dist_setup(n_gpus):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
+        ndev = torch.cuda.device_count()
+        dev = local % ndev
+        torch.cuda.set_device(dev)
+        if ndev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:   # ranks share a GPU (a 1-GPU check of the multi-rank path): NCCL needs distinct GPUs
+            dist.init_process_group("gloo")
+        return world, rank, dev
+    if torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
 
@@ -138,7 +144,8 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    v = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    v = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(v, op=dist.ReduceOp.MAX)
     return float(v.item())
 
