@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C4", "C5"])
+    ap.add_argument("--nan-mode", default="fill", choices=["fill", "mask"],
+                    help="fill: the reference's gap fill (headline); mask: per-pixel masked fits (extension)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -157,11 +159,17 @@ def barrier(world):
         dist.barrier()
 
 
-def cpu_baseline(w, t, sample_px, threads):
+def cpu_baseline(w, t, sample_px, threads, nan_mode="fill"):
     """Oracle port of the reference fused backend (float64 numpy) on a bounded sample."""
     from oracle import bfast_oracle as bo
     from paper_1807_01751_b200.synth import host_stack
 
+    if nan_mode == "mask":                  # per-pixel float64 loop: a small sample, one thread
+        y = host_stack(sample_px, t, w.freq, w.n_hist, w.nan_frac, seed=99)
+        t0 = time.perf_counter()
+        bo.monitor_masked(y, t, w.n_hist, w.bandwidth, w.harmonics, w.freq, w.crit)
+        dt = time.perf_counter() - t0
+        return sample_px / dt / 1e6, dt
     y = host_stack(sample_px, t, w.freq, w.n_hist, w.nan_frac, seed=99)
     bo.monitor(y[:, :4096], t, w.n_hist, w.bandwidth, w.harmonics, w.freq, w.crit, threads=threads)  # warm
     t0 = time.perf_counter()
@@ -222,7 +230,7 @@ def run_ours(args):
     w = WORKLOADS[args.workload]
     t = time_axis(w)
     P = w.n_pixels
-    plan = DevicePlan(TimeAxis(t), w.freq, w.harmonics, w.n_hist, w.bandwidth, w.crit, dev)
+    plan = DevicePlan(TimeAxis(t), w.freq, w.harmonics, w.n_hist, w.bandwidth, w.crit, dev, nan_mode=args.nan_mode)
     y = device_stack(P, t, w.freq, w.n_hist, w.nan_frac, seed=20261017 + rank, device=dev)
     torch.cuda.synchronize()
     res = plan.run_device(y)                    # allocates the output maps once
@@ -274,7 +282,7 @@ def run_ours(args):
         ynp = host.numpy()
         stack = SeriesStack(ynp, TimeAxis(t))
         cfg = MonitorConfig(history=w.n_hist, bandwidth=w.bandwidth, harmonics=w.harmonics, freq=w.freq,
-                            crit_value=w.crit)
+                            crit_value=w.crit, nan_mode=args.nan_mode)
         bm = monitor_batch(stack, cfg)          # warm: pipeline buffers, plan cache, pinned outputs
         barrier(world)
         t0 = time.perf_counter()
@@ -293,15 +301,21 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        v, dt = cpu_baseline(w, t, args.cpu_sample, threads)
+        if args.nan_mode == "mask":
+            sample, threads = min(args.cpu_sample, 4096), 1
+            v, dt = cpu_baseline(w, t, sample, threads, "mask")
+            what = "masked-mode oracle (oracle/bfast_oracle.py:monitor_masked, per-pixel float64)"
+        else:
+            sample = args.cpu_sample
+            v, dt = cpu_baseline(w, t, sample, threads)
+            what = "float64 oracle port of the reference fused backend (oracle/bfast_oracle.py)"
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{args.cpu_sample} px of the {w.name} geometry ({dt:.1f} s), float64 oracle port of "
-                         "the reference fused backend (oracle/bfast_oracle.py)"}
+               "sample": f"{sample} px of the {w.name} geometry ({dt:.1f} s), {what}"}
 
     traffic = None
     prof = REPO / "profiles" / "traffic.json"
     if prof.exists():
-        d = json.loads(prof.read_text()).get(w.name)
+        d = json.loads(prof.read_text()).get(w.name + ("-mask" if args.nan_mode == "mask" else ""))
         if d:
             traffic = d["dram_bytes_per_launch"]
 
@@ -313,6 +327,7 @@ def run_ours(args):
             "data": "synthetic NDVI-like stack generated in HBM (torch Philox), seed 20261017+rank",
             "config": {"workload": f"{w.name}: {w.rows}x{w.cols} px per GPU, N={w.n_obs} dates, n={w.n_hist}, "
                                    f"k={w.harmonics}, h={w.bandwidth}, {int(w.nan_frac * 100)}% NaN",
+                       "nan_mode": args.nan_mode,
                        "pixels_total": world * P, "lambda": w.crit,
                        "l2": f"input {w.n_obs * P * 4 / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush needed)",
                        "parallelism": f"pixel tiles, {world} rank(s), no collective on the data path"},

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BWM_ABI_VERSION 3
+#define BWM_ABI_VERSION 4
 
 /* error codes (negative); positive returns are cudaError_t values */
 #define BWM_OK 0
@@ -54,7 +54,22 @@ typedef struct bwm_dims {
     int32_t n_hist;     /* n : stable history length, p < n < N                     */
     int32_t bandwidth;  /* h : MOSUM window (integer count), 1 <= h <= n            */
     int32_t n_params;   /* p = 2 + 2k : intercept, trend, k sin/cos pairs           */
+    int32_t nan_mode;   /* BWM_NAN_FILL (reference behaviour) or BWM_NAN_MASK        */
 } bwm_dims;
+
+/*
+ * Missing-value handling.
+ *   BWM_NAN_FILL: forward/back fill before fitting — the reference (engine.py:305-319).
+ *   BWM_NAN_MASK: each pixel is fitted on its valid history dates only and monitored over
+ *     its compacted valid series with n_v valid history dates, bandwidth h_v = floor(h n_v / n)
+ *     and boundary lambda sqrt(log_plus((n_v+1+j)/n_v)), lambda = bound[0]; first_idx is the
+ *     1-based offset (from n) of the ORIGINAL date that completes the first crossing window.
+ *     Pixels with n_v <= p, h_v < 1, no valid monitoring date or a singular valid design are
+ *     invalid.  With no missing values both modes give the same result.  (
+ *     the reference has no such mode: oracle/bfast_oracle.py:monitor_masked defines it.)
+ */
+#define BWM_NAN_FILL 0
+#define BWM_NAN_MASK 1
 
 /*
  * Host-side float64 constants for one batch geometry.  The kernel runs in a
@@ -77,7 +92,8 @@ typedef struct bwm_outputs {
     float* max_abs;          /* [P]  max_j |MO_j|                                                  */
     float* beta;             /* [p][ld_out] or NULL: history coefficients, raw basis (model.py:90) */
     float* mo_mean;          /* [P] or NULL: mean_j MO_j                                           */
-    float* mosum;            /* [N-n][ld_out] or NULL: the MOSUM process (keep_mosum)              */
+    float* mosum;            /* [N-n][ld_out] or NULL: the MOSUM process (keep_mosum); mask mode:  */
+                             /*   row t-n holds the window ending at date t, NaN on missing dates */
     int64_t ld_out;          /* leading dimension of beta / mosum (>= P)                           */
     /* lowest global pixel index whose history fits exactly (sigma == 0); caller initialises
        to INT64_MAX (device pointer for bwm_monitor, host pointer for bwm_monitor_host).
@@ -136,6 +152,10 @@ typedef struct bwm_plan_info_t {
     int32_t ctas_per_sm_ldg;  /* persistent CTAs per SM, LDG kernel                                  */
     int32_t occupancy_tma;    /* occupancy-API result for the TMA kernel                             */
     int32_t force_ldg;        /* BWM_KERNEL=ldg was set at plan creation                             */
+    int32_t nan_mode;         /* BWM_NAN_FILL / BWM_NAN_MASK                                         */
+    int32_t masked_global;    /* mask mode: x x^T table and residual rings in global memory          */
+    int32_t ctas_per_sm_masked;
+    int64_t smem_masked;      /* dynamic shared memory per CTA, masked kernel                        */
 } bwm_plan_info_t;
 
 int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info);

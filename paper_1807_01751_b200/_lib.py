@@ -20,7 +20,12 @@ BWM_E_PARAMS = -3
 BWM_E_SMEM = -4
 BWM_E_DEVICE = -5
 
+BWM_NAN_FILL = 0
+BWM_NAN_MASK = 1
+NAN_MODES = {"fill": BWM_NAN_FILL, "mask": BWM_NAN_MASK}
+
 INT64_MAX = (1 << 63) - 1
+ABI_VERSION = 4
 
 
 class Dims(C.Structure):
@@ -29,6 +34,7 @@ class Dims(C.Structure):
         ("n_hist", C.c_int32),
         ("bandwidth", C.c_int32),
         ("n_params", C.c_int32),
+        ("nan_mode", C.c_int32),
     ]
 
 
@@ -62,6 +68,8 @@ class PlanInfo(C.Structure):
         ("ring_mode", C.c_int32), ("ring_rows", C.c_int32), ("tmem_cols", C.c_int32), ("sms", C.c_int32),
         ("smem_tma", C.c_int64), ("smem_ldg", C.c_int64), ("ctas_per_sm_tma", C.c_int32),
         ("ctas_per_sm_ldg", C.c_int32), ("occupancy_tma", C.c_int32), ("force_ldg", C.c_int32),
+        ("nan_mode", C.c_int32), ("masked_global", C.c_int32), ("ctas_per_sm_masked", C.c_int32),
+        ("smem_masked", C.c_int64),
     ]
 
 
@@ -101,7 +109,7 @@ def load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.bwm_abi_version() != 3:
+    if lib.bwm_abi_version() != ABI_VERSION:
         raise RuntimeError("libbwm ABI version mismatch; rebuild the library")
     _lib = lib
     return lib

@@ -28,6 +28,15 @@ BWM_DECLARE_PICK(12)
 BWM_DECLARE_PICK(14)
 BWM_DECLARE_PICK(16)
 BWM_DECLARE_PICK(18)
+#define BWM_DECLARE_PICK_MASKED(NP) bwm::KernelFn bwm_pick_masked_p##NP(int big);
+BWM_DECLARE_PICK_MASKED(4)
+BWM_DECLARE_PICK_MASKED(6)
+BWM_DECLARE_PICK_MASKED(8)
+BWM_DECLARE_PICK_MASKED(10)
+BWM_DECLARE_PICK_MASKED(12)
+BWM_DECLARE_PICK_MASKED(14)
+BWM_DECLARE_PICK_MASKED(16)
+BWM_DECLARE_PICK_MASKED(18)
 
 namespace bwm {
 cudaError_t launch_finalize(const int32_t* first_idx, const float* max_abs, int64_t P, int n, int64_t* first_break,
@@ -162,6 +171,23 @@ KernelFn pick(int p, Kind kind, int mode) {
     }
 }
 
+KernelFn pick_masked(int p, bool big) {
+    switch (p) {
+        case 4: return bwm_pick_masked_p4(big);
+        case 6: return bwm_pick_masked_p6(big);
+        case 8: return bwm_pick_masked_p8(big);
+        case 10: return bwm_pick_masked_p10(big);
+        case 12: return bwm_pick_masked_p12(big);
+        case 14: return bwm_pick_masked_p14(big);
+        case 16: return bwm_pick_masked_p16(big);
+        case 18: return bwm_pick_masked_p18(big);
+        default: return nullptr;
+    }
+}
+
+// masked kernel: x x^T table and rings in shared memory up to this size, else global (BIG)
+constexpr int64_t kMaskedSmemMax = 96 << 10;
+
 int threads_of(Kind k) { return k == kTma ? bwm::kTmaThreads : bwm::kThreads; }
 
 }  // namespace
@@ -197,7 +223,7 @@ struct bwm_plan {
     float* d_xt = nullptr;
     float* d_bound = nullptr;
     float* d_rinv = nullptr;
-    float inv_dof = 0, sqrt_n = 0, tc_ts = 0, inv_ts = 0;
+    float inv_dof = 0, sqrt_n = 0, tc_ts = 0, inv_ts = 0, lambda = 0;
     bool ring = true;                  // LDG kernels: smem ring (else lagging cursor)
     TmaRing tring{};                   // TMA kernel ring mode
     int64_t smem = 0;                  // LDG kernels
@@ -206,6 +232,14 @@ struct bwm_plan {
     int blocks_per_sm[3] = {0, 0, 0};  // [Kind]
     int occ_raw[3] = {0, 0, 0};        // occupancy API result before the TMEM cap
     bool force_ldg = false;            // BWM_KERNEL=ldg (A/B against the TMA kernel)
+    // masked-NaN mode (bwm_kernel_masked.cuh)
+    bool masked = false;
+    bool mbig = false;                 // x x^T table + rings in global memory
+    int64_t smem_masked = 0;
+    int bpm_masked = 0;
+    float* d_xx = nullptr;
+    double* d_gfull = nullptr;
+    float* d_ring = nullptr;           // [sms * bpm_masked][h][128] when mbig
     HostPipe pipe;
     std::mutex mu;                     // serialises bwm_monitor_host on one plan
 };
@@ -220,9 +254,84 @@ static int validate_dims(const bwm_dims* d) {
     if (!(d->n_hist < d->n_obs))
         return set_err(BWM_E_DIMS, "history must end before the series does (n=%d, N=%d)",
                        d->n_hist, d->n_obs);
+    if (d->nan_mode != BWM_NAN_FILL && d->nan_mode != BWM_NAN_MASK)
+        return set_err(BWM_E_PARAMS, "nan_mode=%d is neither BWM_NAN_FILL nor BWM_NAN_MASK", d->nan_mode);
     if (d->bandwidth < 1 || d->bandwidth > d->n_hist)
         return set_err(BWM_E_DIMS, "bandwidth must satisfy 1 <= h <= n (h=%d, n=%d)", d->bandwidth,
                        d->n_hist);
+    return BWM_OK;
+}
+
+static void plan_free_tables(bwm_plan* plan) {
+    cudaFree(plan->d_mt);
+    cudaFree(plan->d_xt);
+    cudaFree(plan->d_bound);
+    cudaFree(plan->d_rinv);
+    cudaFree(plan->d_xx);
+    cudaFree(plan->d_gfull);
+    cudaFree(plan->d_ring);
+}
+
+
+// Masked-NaN plan: float32 X'^T for residuals, the x_t x_t^T lower triangles of the history
+// dates (zero rows up to the 16-date block), their float64 total G_full (summed from the
+// float32-rounded rows so that G_v = G_full - Gm is the Gram of exactly those rows), lambda.
+static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_optin, bwm_plan** out_plan) {
+    const bwm_dims& d = plan->dims;
+    const int N = d.n_obs, n = d.n_hist, p = d.n_params, h = d.bandwidth, sp = plan->sp;
+    const int kk = p * (p + 1) / 2, kp = (((kk + 1) / 2 * 2 + 3) / 4) * 4;
+    const int n16 = ((n + bwm::kMaskD - 1) / bwm::kMaskD) * bwm::kMaskD;
+    plan->masked = true;
+    const int64_t small = bwm::masked_smem_bytes(N, n, h, p, false);
+    plan->mbig = small > kMaskedSmemMax;
+    plan->smem_masked = bwm::masked_smem_bytes(N, n, h, p, plan->mbig);
+    if (plan->smem_masked > max_optin) {
+        const int64_t need = plan->smem_masked;
+        delete plan;
+        return set_err(BWM_E_SMEM, "masked tables need %lld B of shared memory, device allows %d",
+                       (long long)need, max_optin);
+    }
+    std::vector<float> xt((size_t)N * sp, 0.f), xx((size_t)n16 * kp, 0.f);
+    std::vector<double> gf((size_t)kk, 0.0);
+    for (int t = 0; t < N; ++t)
+        for (int i = 0; i < p; ++i) xt[(size_t)t * sp + i] = (float)tb->design[(size_t)i * N + t];
+    for (int t = 0; t < n; ++t)
+        for (int i = 0; i < p; ++i)
+            for (int j = 0; j <= i; ++j) {
+                const float v = (float)(tb->design[(size_t)i * N + t] * tb->design[(size_t)j * N + t]);
+                xx[(size_t)t * kp + i * (i + 1) / 2 + j] = v;
+                gf[(size_t)i * (i + 1) / 2 + j] += (double)v;
+            }
+    auto fail = [&](cudaError_t e, const char* what) {
+        plan_free_tables(plan);
+        delete plan;
+        return set_err((int)e, "%s: %s", what, cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&plan->d_xt, xt.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&plan->d_xx, xx.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&plan->d_gfull, gf.size() * 8)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMemcpy(plan->d_xt, xt.data(), xt.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy");
+    if ((e = cudaMemcpy(plan->d_xx, xx.data(), xx.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy");
+    if ((e = cudaMemcpy(plan->d_gfull, gf.data(), gf.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy");
+    plan->lambda = (float)tb->bound[0];    // bound_0 = crit * sqrt(log_plus((n+1)/n)) = crit
+    KernelFn fn = pick_masked(p, plan->mbig);
+    if ((e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin)) !=
+        cudaSuccess)
+        return fail(e, "cudaFuncSetAttribute");
+    int nb = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, bwm::kMaskThreads,
+                                                           (size_t)plan->smem_masked)) != cudaSuccess)
+        return fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    plan->bpm_masked = std::max(nb, 1);
+    if (plan->mbig) {
+        const size_t rb = (size_t)plan->sms * plan->bpm_masked * h * bwm::kMaskThreads * 8;   // residual + date
+        if ((e = cudaMalloc(&plan->d_ring, rb)) != cudaSuccess) return fail(e, "cudaMalloc(ring)");
+    }
+    *out_plan = plan;
     return BWM_OK;
 }
 
@@ -235,6 +344,11 @@ int64_t bwm_launch_count(void) { return g_launches.load(); }
 int64_t bwm_smem_bytes(const bwm_dims* d) {
     int rc = validate_dims(d);
     if (rc) return rc;
+    if (d->nan_mode == BWM_NAN_MASK) {
+        const int64_t small = bwm::masked_smem_bytes(d->n_obs, d->n_hist, d->bandwidth, d->n_params, false);
+        return small <= kMaskedSmemMax ? small
+                                       : bwm::masked_smem_bytes(d->n_obs, d->n_hist, d->bandwidth, d->n_params, true);
+    }
     const bool ring = d->bandwidth <= kRingMaxH;
     const int64_t tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, tma_ring_for(d->bandwidth).mode);
     return tma > 0 ? tma : smem_bytes_for(d->n_obs, d->n_hist, d->bandwidth, d->n_params, ring);
@@ -273,6 +387,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     int max_optin = 0;
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device);
+    if (dims->nan_mode == BWM_NAN_MASK) return plan_create_masked(plan, tb, max_optin, out_plan);
     if (plan->smem_tma > max_optin || plan->tring.mode < 0) plan->smem_tma = 0;
     if (plan->smem > max_optin) {
         int64_t need = plan->smem;
@@ -422,10 +537,7 @@ void bwm_plan_destroy(bwm_plan* plan) {
     DeviceRestore guard(plan->device);
     cudaSetDevice(plan->device);
     pipe_free(plan->pipe);
-    cudaFree(plan->d_mt);
-    cudaFree(plan->d_xt);
-    cudaFree(plan->d_bound);
-    cudaFree(plan->d_rinv);
+    plan_free_tables(plan);
     delete plan;
 }
 
@@ -474,6 +586,22 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     k.mosum = out->mosum;
     k.ld_out = out->ld_out;
     k.zero_sigma = reinterpret_cast<unsigned long long*>(out->zero_sigma_pixel);
+    cudaStream_t st = (cudaStream_t)stream;
+    int launched = 0;
+
+    if (plan->masked) {
+        // one launch, any alignment (scalar predicated loads and stores)
+        k.xx = plan->d_xx;
+        k.gfull = plan->d_gfull;
+        k.ring_g = plan->d_ring;
+        k.lambda = plan->lambda;
+        const int64_t tiles = (n_pixels + bwm::kMaskTile - 1) / bwm::kMaskTile;
+        const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * plan->bpm_masked);
+        pick_masked(d.n_params, plan->mbig)<<<(unsigned)grid, bwm::kMaskThreads, (size_t)plan->smem_masked, st>>>(k);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
+        ++launched;
+    }
 
     // Whole 256-pixel tiles go to the TMA kernel (rows 16-byte aligned, outputs 8-byte
     // aligned) or, with BWM_KERNEL=ldg / when its smem does not fit, the LDG fast kernel
@@ -483,13 +611,11 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     const bool out_al = al(out->valid, 2) && al(out->first_idx, 8) && al(out->max_abs, 8) &&
                         (!out->mo_mean || al(out->mo_mean, 8)) && (!out->beta || al(out->beta, 8)) &&
                         (!out->mosum || al(out->mosum, 8)) && (out->ld_out % 2 == 0 || (!out->beta && !out->mosum));
-    const bool tma_ok = !plan->force_ldg && plan->smem_tma > 0 && al(y, 16) && (ld_y % 4 == 0) && out_al;
+    const bool tma_ok = !plan->masked && !plan->force_ldg && plan->smem_tma > 0 && al(y, 16) && (ld_y % 4 == 0) && out_al;
     const bool ldg_ok = al(y, 8) && (ld_y % 2 == 0);
     const Kind main_kind = tma_ok ? kTma : kLdgFast;
     const int64_t full = (tma_ok || ldg_ok) ? (n_pixels / bwm::kTile) * bwm::kTile : 0;
-    cudaStream_t st = (cudaStream_t)stream;
-    int launched = 0;
-    for (int part = 0; part < 2; ++part) {
+    for (int part = 0; part < 2 && !plan->masked; ++part) {
         const Kind kind = part == 0 ? main_kind : kLdgSafe;
         const int64_t p0 = part == 0 ? 0 : full;
         const int64_t cnt = part == 0 ? full : n_pixels - full;
@@ -741,6 +867,10 @@ int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {
     info->occupancy_tma = plan->occ_raw[kTma];
     info->sms = plan->sms;
     info->force_ldg = plan->force_ldg ? 1 : 0;
+    info->nan_mode = plan->dims.nan_mode;
+    info->masked_global = plan->mbig ? 1 : 0;
+    info->ctas_per_sm_masked = plan->bpm_masked;
+    info->smem_masked = plan->smem_masked;
     return BWM_OK;
 }
 

@@ -6,7 +6,7 @@
 //     leading back-fill becomes exactly 0);
 //   * the trend regressor is centred/scaled on the host (M', X': a reparametrisation that
 //     leaves fitted values unchanged in exact arithmetic);
-//   * 16-date FFMA2 block partials are 2Sum-compensated into (hi, lo).
+//   * 32-date FFMA2 block partials are 2Sum-compensated into (hi, lo).
 #pragma once
 #include <cuda.h>
 #include <type_traits>
@@ -45,6 +45,11 @@ struct KParams {
     float* mosum;
     int64_t ld_out;
     unsigned long long* zero_sigma;   // atomicMin target (int64 bit pattern, non-negative)
+    // masked-NaN mode (bwm_kernel_masked.cuh); xt then holds X'^T (the centred raw design)
+    const float* xx;            // [n16][KP] x_t x_t^T lower triangles of the history dates, zero padded
+    const double* gfull;        // [KK] sum of those rows over the whole history
+    float* ring_g;              // per-CTA residual rings [grid][h][128] when they live in global memory
+    float lambda;               // crit = bound[0]
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -114,7 +119,7 @@ __device__ __forceinline__ void axpy_row(float2 (&part)[NP], float2 vc, const fl
 }
 
 // Residual sum of squares of the history fit in the orthonormal basis (one pass):
-// RSS = ||y_h - c||^2 - ||beta_Q||^2, accumulated in float64 (q from 16-date float32 block
+// RSS = ||y_h - c||^2 - ||beta_Q||^2, accumulated in float64 (q from 32-date float32 block
 // partials).  Clamped at 0: a (near-)exact fit is a zero-sigma pixel.
 template <int NP>
 __device__ __forceinline__ float2 rss_onepass(double q0, double q1, const float2 (&bq)[NP]) {

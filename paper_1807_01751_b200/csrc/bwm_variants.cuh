@@ -2,6 +2,7 @@
 #pragma once
 #include "bwm_kernel_ldg.cuh"
 #include "bwm_kernel_tma.cuh"
+#include "bwm_kernel_masked.cuh"
 
 namespace bwm {
 enum Kind { kLdgFast = 0, kLdgSafe = 1, kTma = 2 };
@@ -23,4 +24,11 @@ using KernelFn = void (*)(const KParams);
                 return mode == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem>      \
                                               : bwm::monitor_kernel_tma<NP, bwm::kRingLag>;      \
         }                                                                                        \
+    }
+
+// Defines bwm::KernelFn bwm_pick_masked_p<NP>(int big): the masked-NaN kernel with its x x^T
+// table and residual rings in shared memory (big = 0) or global memory (big = 1).
+#define BWM_DEFINE_PICK_MASKED(NP)                                                               \
+    bwm::KernelFn bwm_pick_masked_p##NP(int big) {                                               \
+        return big ? bwm::monitor_kernel_masked<NP, true> : bwm::monitor_kernel_masked<NP, false>; \
     }

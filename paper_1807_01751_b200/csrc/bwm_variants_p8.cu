@@ -2,3 +2,4 @@
 #include "bwm_variants.cuh"
 
 BWM_DEFINE_PICK(8)
+BWM_DEFINE_PICK_MASKED(8)

@@ -88,8 +88,11 @@ class DevicePlan:
     _lock = threading.Lock()
 
     def __init__(self, axis: TimeAxis, freq: float, harmonics: int, n_hist: int, bandwidth: int,
-                 crit: float, device=None):
+                 crit: float, device=None, nan_mode: str = "fill"):
         lib = _lib.load()
+        if nan_mode not in _lib.NAN_MODES:
+            raise ValueError(f"nan_mode must be one of {sorted(_lib.NAN_MODES)}, got {nan_mode!r}")
+        self.nan_mode = nan_mode
         self.torch_device = _as_torch_device(device)
         self.n_obs = len(axis)
         self.n_hist = int(n_hist)
@@ -99,7 +102,7 @@ class DevicePlan:
         basis = kernel_basis(axis, freq, harmonics, n_hist)
         bound = boundary_values(n_hist, self.n_obs, crit)
         self._keep = (basis, bound)
-        self.dims = _lib.Dims(self.n_obs, self.n_hist, self.bandwidth, self.n_params)
+        self.dims = _lib.Dims(self.n_obs, self.n_hist, self.bandwidth, self.n_params, _lib.NAN_MODES[nan_mode])
         dbl = C.POINTER(C.c_double)
         tables = _lib.Tables(
             basis.design.ctypes.data_as(dbl),
@@ -123,13 +126,14 @@ class DevicePlan:
 
     @classmethod
     def get(cls, axis: TimeAxis, freq: float, harmonics: int, n_hist: int, bandwidth: int,
-            crit: float, device=None) -> "DevicePlan":
+            crit: float, device=None, nan_mode: str = "fill") -> "DevicePlan":
         dev = _as_torch_device(device)
-        key = (_axis_key(axis), float(freq), int(harmonics), int(n_hist), int(bandwidth), float(crit), dev.index)
+        key = (_axis_key(axis), float(freq), int(harmonics), int(n_hist), int(bandwidth), float(crit), dev.index,
+               nan_mode)
         with cls._lock:
             plan = cls._cache.get(key)
             if plan is None:
-                plan = cls(axis, freq, harmonics, n_hist, bandwidth, crit, dev)
+                plan = cls(axis, freq, harmonics, n_hist, bandwidth, crit, dev, nan_mode)
                 if len(cls._cache) > 16:
                     cls._cache.clear()
                 cls._cache[key] = plan
@@ -140,7 +144,8 @@ class DevicePlan:
         pi = _lib.PlanInfo()
         _lib.check(self._lib.bwm_plan_info(self._handle, C.byref(pi)), "bwm_plan_info")
         d = {name: getattr(pi, name) for name, _ in _lib.PlanInfo._fields_}
-        d["ring_mode"] = {0: "smem", 1: "tmem", 2: "lag"}[d["ring_mode"]]
+        d["ring_mode"] = {-1: "none", 0: "smem", 1: "tmem", 2: "lag"}[d["ring_mode"]]
+        d["nan_mode"] = {v: k for k, v in _lib.NAN_MODES.items()}[d["nan_mode"]]
         return d
 
     # ------------------------------------------------------------------ device path

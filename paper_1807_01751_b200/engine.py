@@ -41,6 +41,7 @@ CALIBRATION_REPS = 50_000
 CALIBRATION_SEED = 7
 PHASE_NAMES = ("ingest", "model", "predictions", "residuals", "mosum", "breaks")
 BACKENDS = ("fused", "cuda")
+NAN_MODES = ("fill", "mask")
 
 
 def resolve_threads(threads: Optional[int] = None) -> int:
@@ -121,6 +122,10 @@ class MonitorConfig:
     alpha: float = 0.05
     crit_value: Optional[float] = None
     backend: str = "fused"
+    # "fill": the reference's forward/back gap fill (engine.py:305-319).  "mask": each pixel
+    # is fitted on its valid history dates and monitored over its compacted valid series
+    # (include/bwm.h BWM_NAN_MASK) — an extension, not in the reference.
+    nan_mode: str = "fill"
 
     def __post_init__(self):
         if self.harmonics < 1:
@@ -135,6 +140,8 @@ class MonitorConfig:
             raise ValueError("alpha must lie in (0, 1)")
         if self.crit_value is not None and not self.crit_value > 0:
             raise ValueError("explicit critical value must be positive")
+        if self.nan_mode not in NAN_MODES:
+            raise ValueError(f"nan_mode must be 'fill' or 'mask', got {self.nan_mode!r}")
         if self.backend not in BACKENDS:
             raise ValueError(
                 "backend must be 'fused' or 'cuda' (the reference's 'naive' per-pixel CPU "
@@ -252,7 +259,7 @@ def _run(stack, config, threads, block_size, keep_mosum, return_beta, return_mea
     if _is_cuda_tensor(stack.data) and device is None:
         device = stack.data.device
     plan = DevicePlan.get(stack.time_axis, config.freq, config.harmonics, config.history,
-                          config.bandwidth, crit, device)
+                          config.bandwidth, crit, device, nan_mode=config.nan_mode)
     t_model = clock() - mark
 
     n = config.history

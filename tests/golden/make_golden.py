@@ -32,6 +32,7 @@ import breakwatch as bw  # noqa: E402  (the reference)
 
 from oracle.bfast_oracle import near_pairs  # noqa: E402
 from paper_1807_01751_b200.synth import WORKLOADS, host_stack, time_axis  # noqa: E402
+from tests.golden_cases import edge_stack  # noqa: E402
 
 STORE_INPUT_MAX = 1 << 20   # bytes
 
@@ -75,25 +76,6 @@ def save(name, y, t, n, h, k, f, crit, meta=None, store_input=None):
                 breaks=int(bm.break_count), **(meta or {}))
     np.savez_compressed(HERE / f"{name}.npz", info=json.dumps(info), **arrays)
     print(f"{name}: shape={y.shape} breaks={bm.break_count} near={len(arrays['near'])} stored_input={store}")
-
-
-def edge_stack(rng, N, P, n):
-    y = (0.5 + 0.1 * rng.standard_normal((N, P))).astype(np.float32)
-    y[:, 0] = np.nan                                  # dead pixel
-    y[:3, 1] = np.nan                                 # short leading gap
-    y[:17, 2] = np.nan                                # leading gap longer than a stage
-    y[:40, 3] = np.nan                                # leading gap inside the history
-    y[:n + 5, 4] = np.nan                             # first finite value in the monitor period
-    y[-7:, 5] = np.nan                                # trailing gap
-    y[10, 6], y[11, 6], y[12, 6] = np.inf, -np.inf, np.nan   # infinities count as gaps
-    y[n - 3:n + 3, 7] = np.nan                        # gap across the history boundary
-    y[::2, 8] = np.nan                                # every other date missing
-    y[:-1, 9] = np.nan                                # only the last date finite
-    y[1:, 10] = np.nan                                # only the first date finite
-    mask = rng.random((N, P)) < 0.3
-    mask[:, :12] = False
-    y[mask] = np.nan
-    return y
 
 
 def main():
@@ -169,5 +151,59 @@ def main():
     }, indent=1))
 
 
+def save_masked_common(name, y, t, n, h, k, f, crit, keep):
+    """Masked-mode fixture with gaps on the SAME dates in every pixel: the reference, run on
+    the compacted series (dates `keep`, history n_v = #kept dates < n, bandwidth
+    h_v = floor(h n_v / n)), gives what masked mode must return — the breaks mapped back to
+    the original dates and the MOSUM rows to the kept monitoring dates."""
+    keep = np.asarray(keep)
+    yk, tk = y[keep], t[keep]
+    n_v = int(np.sum(keep < n))
+    h_v = (h * n_v) // n
+    bm, beta, _ = run_reference(yk, tk, n_v, h_v, k, f, crit)
+    N = y.shape[0]
+    mon = keep[n_v:]                                  # original monitoring dates kept
+    first = np.where(bm.first_break > 0, mon[np.maximum(bm.first_break - n_v - 1, 0)] + 1, 0)
+    mosum = np.full((N - n, y.shape[1]), np.nan, dtype=np.float32)
+    mosum[mon - n] = bm.mosum
+    arrays = dict(t=t, y=y, first_break=first.astype(np.int32), max_abs_mo=bm.max_abs_mo, valid=bm.valid,
+                  mosum_mean=bm.mosum.mean(axis=0), beta=beta, mosum=mosum, keep=keep,
+                  near=near_pairs(bm.mosum, bw.boundary_values(n_v, len(keep), crit)),
+                  bound=bw.boundary_values(n, N, crit))
+    info = dict(n=n, h=h, k=k, freq=f, crit=crit, shape=list(y.shape), y_sha256=sha(y),
+                breaks=int(bm.break_count), nan_mode="mask", n_v=n_v, h_v=h_v,
+                source="reference on the compacted series")
+    np.savez_compressed(HERE / f"{name}.npz", info=json.dumps(info), **arrays)
+    print(f"{name}: shape={y.shape} n_v={n_v} h_v={h_v} breaks={bm.break_count}")
+
+
+def masked():
+    """Fixtures for nan_mode="mask", pinned by the reference itself."""
+    # NaN-free input: masked == fill == reference
+    t = np.arange(1.0, 229.0)
+    y = host_stack(1000, t, 23.0, 114, 0.0, seed=31, dead_frac=0.0)
+    save("mask_nanfree", y, t, 114, 28, 3, 23.0, 2.96519227, {"nan_mode": "mask", "seed": 31})
+    # gaps on common dates
+    rng = np.random.default_rng(32)
+    y = host_stack(1000, t, 23.0, 114, 0.0, seed=32, dead_frac=0.0)
+    keep = np.sort(rng.choice(228, size=171, replace=False))
+    y[np.setdiff1d(np.arange(228), keep)] = np.nan
+    save_masked_common("mask_common_c1", y, t, 114, 28, 3, 23.0, 2.96519227, keep)
+    tt = np.cumsum(np.random.default_rng(33).uniform(8.0, 24.0, 400)) + 1.0
+    y = host_stack(700, tt, 365.25, 200, 0.0, seed=33, dead_frac=0.0)
+    keep = np.flatnonzero(np.random.default_rng(34).random(400) > 0.35)
+    y[np.setdiff1d(np.arange(400), keep)] = np.nan
+    save_masked_common("mask_common_irregular", y, tt, 200, 50, 3, 365.25, 3.0, keep)
+    t = np.arange(1.0, 121.0)
+    y = host_stack(300, t, 40.0, 60, 0.0, seed=35, dead_frac=0.0)
+    keep = np.flatnonzero(np.random.default_rng(36).random(120) > 0.5)
+    y[np.setdiff1d(np.arange(120), keep)] = np.nan
+    save_masked_common("mask_common_k8_h60", y, t, 60, 60, 8, 40.0, 2.7, keep)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["masked"]:
+        masked()
+    else:
+        main()
+        masked()

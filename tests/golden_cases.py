@@ -65,3 +65,22 @@ def load(name: str) -> Case:
     return Case(name, y, t, info["n"], info["h"], info["k"], info["freq"], info["crit"],
                 z["first_break"].astype(np.int64), z["max_abs_mo"], z["valid"], z["near"], z["bound"],
                 z["mosum_mean"], z["beta"] if "beta" in z else None, z["mosum"] if "mosum" in z else None, info)
+
+
+def edge_stack(rng, N, P, n):
+    y = (0.5 + 0.1 * rng.standard_normal((N, P))).astype(np.float32)
+    y[:, 0] = np.nan                                  # dead pixel
+    y[:3, 1] = np.nan                                 # short leading gap
+    y[:17, 2] = np.nan                                # leading gap longer than a stage
+    y[:40, 3] = np.nan                                # leading gap inside the history
+    y[:n + 5, 4] = np.nan                             # first finite value in the monitor period
+    y[-7:, 5] = np.nan                                # trailing gap
+    y[10, 6], y[11, 6], y[12, 6] = np.inf, -np.inf, np.nan   # infinities count as gaps
+    y[n - 3:n + 3, 7] = np.nan                        # gap across the history boundary
+    y[::2, 8] = np.nan                                # every other date missing
+    y[:-1, 9] = np.nan                                # only the last date finite
+    y[1:, 10] = np.nan                                # only the first date finite
+    mask = rng.random((N, P)) < 0.3
+    mask[:, :12] = False
+    y[mask] = np.nan
+    return y

@@ -42,7 +42,7 @@ def test_abi_version_and_error_string():
     from paper_1807_01751_b200 import _lib
 
     lib = _lib.load()
-    assert lib.bwm_abi_version() == 3
+    assert lib.bwm_abi_version() == _lib.ABI_VERSION == 4
     assert isinstance(lib.bwm_last_error(), bytes)
 
 
@@ -57,6 +57,9 @@ def test_abi_version_and_error_string():
         ((228, 8, 4, 8), -2),               # n <= p
         ((228, 114, 28, 7), -3),            # odd parameter count
         ((228, 114, 28, 20), -3),           # k > 8
+        ((228, 114, 28, 8, 1), None),       # masked-NaN mode, tables in shared memory
+        ((1000, 500, 250, 14, 1), None),    # masked-NaN mode, x x^T table + rings in global memory
+        ((228, 114, 28, 8, 2), -3),         # unknown nan_mode
     ],
 )
 def test_dimension_validation(dims, code):
