@@ -273,13 +273,44 @@ static void plan_free_tables(bwm_plan* plan) {
 }
 
 
-// Masked-NaN plan: float32 X'^T for residuals, the x_t x_t^T lower triangles of the history
-// dates (zero rows up to the 16-date block), their float64 total G_full (summed from the
-// float32-rounded rows so that G_v = G_full - Gm is the Gram of exactly those rows), lambda.
+// CTAs per SM for a kernel that allocates Tensor Memory dynamically: the occupancy API
+// assumes such a kernel owns the SM's TMEM (reports 1), so bound residency by registers,
+// shared memory, threads and our own column budget (512 columns / tmem_cols per CTA).
+static int resident_ctas(const void* fn, int threads, int64_t smem, int tmem_cols, int device, cudaError_t* err) {
+    cudaFuncAttributes fa{};
+    if ((*err = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return 0;
+    int regs_per_sm = 0, smem_per_sm = 0, reserved = 0, max_threads = 0;
+    cudaDeviceGetAttribute(&regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, device);
+    cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+    cudaDeviceGetAttribute(&max_threads, cudaDevAttrMaxThreadsPerMultiProcessor, device);
+    const int warps = (threads + 31) / 32;
+    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;     // per-warp allocation unit
+    const int by_regs = regs_per_sm / (regs_warp * warps);
+    const int by_smem = (int)(smem_per_sm / (smem + (int64_t)fa.sharedSizeBytes + reserved));
+    const int by_thr = max_threads / threads;
+    const int by_tmem = 512 / tmem_cols;
+    return std::max(1, std::min(std::min(by_regs, by_smem), std::min(by_thr, by_tmem)));
+}
+
+// round to the nearest tf32 (10 explicit mantissa bits), as a float32 bit pattern
+static float tf32_round(float x) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    if ((b & 0x7f800000u) != 0x7f800000u) b = (b + 0xfffu + ((b >> 13) & 1u)) & 0xffffe000u;
+    std::memcpy(&x, &b, 4);
+    return x;
+}
+
+// Masked-NaN plan: float32 X'^T for residuals; the x_t x_t^T lower triangles of the history
+// dates as tf32 hi + lo tiles in the tensor-core operand layout (bwm_kernel_masked.cuh: per
+// 16-date block, [step][hi|lo][N/8 row groups][2 K chunks][8 rows][4 dates], zero padded);
+// their float64 total G_full (summed from the same hi + lo values, so G_v = G_full - Gm is
+// the Gram of exactly those rows); lambda.
 static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_optin, bwm_plan** out_plan) {
     const bwm_dims& d = plan->dims;
     const int N = d.n_obs, n = d.n_hist, p = d.n_params, h = d.bandwidth, sp = plan->sp;
-    const int kk = p * (p + 1) / 2, kp = (((kk + 1) / 2 * 2 + 3) / 4) * 4;
+    const int kk = p * (p + 1) / 2, nn = bwm::gram_nn(p);
     const int n16 = ((n + bwm::kMaskD - 1) / bwm::kMaskD) * bwm::kMaskD;
     plan->masked = true;
     const int64_t small = bwm::masked_smem_bytes(N, n, h, p, false);
@@ -291,17 +322,28 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
         return set_err(BWM_E_SMEM, "masked tables need %lld B of shared memory, device allows %d",
                        (long long)need, max_optin);
     }
-    std::vector<float> xt((size_t)N * sp, 0.f), xx((size_t)n16 * kp, 0.f);
+    if (n16 > 65535 || N > 65535) {
+        delete plan;
+        return set_err(BWM_E_DIMS, "masked mode supports at most 65535 dates");
+    }
+    std::vector<float> xt((size_t)N * sp, 0.f), tiles((size_t)(n16 / bwm::kMaskD) * nn * 32, 0.f);
     std::vector<double> gf((size_t)kk, 0.0);
     for (int t = 0; t < N; ++t)
         for (int i = 0; i < p; ++i) xt[(size_t)t * sp + i] = (float)tb->design[(size_t)i * N + t];
-    for (int t = 0; t < n; ++t)
+    for (int t = 0; t < n; ++t) {
+        const int kb = t / bwm::kMaskD, step = (t % bwm::kMaskD) / 8, k = t % 8;
         for (int i = 0; i < p; ++i)
             for (int j = 0; j <= i; ++j) {
+                const int e = i * (i + 1) / 2 + j;
                 const float v = (float)(tb->design[(size_t)i * N + t] * tb->design[(size_t)j * N + t]);
-                xx[(size_t)t * kp + i * (i + 1) / 2 + j] = v;
-                gf[(size_t)i * (i + 1) / 2 + j] += (double)v;
+                const float hi = tf32_round(v), lo = tf32_round(v - hi);
+                const size_t in_region = (size_t)(e / 8) * 64 + (k / 4) * 32 + (e % 8) * 4 + (k % 4);
+                const size_t base = (size_t)kb * nn * 32 + (size_t)(2 * step) * nn * 8;
+                tiles[base + in_region] = hi;
+                tiles[base + (size_t)nn * 8 + in_region] = lo;
+                gf[e] += (double)hi + (double)lo;
             }
+    }
     auto fail = [&](cudaError_t e, const char* what) {
         plan_free_tables(plan);
         delete plan;
@@ -309,11 +351,11 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
     };
     cudaError_t e;
     if ((e = cudaMalloc(&plan->d_xt, xt.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
-    if ((e = cudaMalloc(&plan->d_xx, xx.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&plan->d_xx, tiles.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&plan->d_gfull, gf.size() * 8)) != cudaSuccess) return fail(e, "cudaMalloc");
     if ((e = cudaMemcpy(plan->d_xt, xt.data(), xt.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
-    if ((e = cudaMemcpy(plan->d_xx, xx.data(), xx.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+    if ((e = cudaMemcpy(plan->d_xx, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
     if ((e = cudaMemcpy(plan->d_gfull, gf.data(), gf.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
@@ -322,13 +364,11 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
     if ((e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin)) !=
         cudaSuccess)
         return fail(e, "cudaFuncSetAttribute");
-    int nb = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, bwm::kMaskThreads,
-                                                           (size_t)plan->smem_masked)) != cudaSuccess)
-        return fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    plan->bpm_masked = std::max(nb, 1);
+    plan->bpm_masked = resident_ctas((const void*)fn, bwm::kMaskThreads, plan->smem_masked,
+                                     bwm::masked_tmem_cols(p), plan->device, &e);
+    if (e != cudaSuccess) return fail(e, "cudaFuncGetAttributes");
     if (plan->mbig) {
-        const size_t rb = (size_t)plan->sms * plan->bpm_masked * h * bwm::kMaskThreads * 8;   // residual + date
+        const size_t rb = (size_t)plan->sms * plan->bpm_masked * bwm::masked_scratch_words(h, p) * bwm::kMaskThreads * 4;
         if ((e = cudaMalloc(&plan->d_ring, rb)) != cudaSuccess) return fail(e, "cudaMalloc(ring)");
     }
     *out_plan = plan;

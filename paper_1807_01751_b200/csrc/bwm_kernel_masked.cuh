@@ -13,11 +13,16 @@
 //
 // Layout: one pixel per thread (128-pixel tiles, 128 threads), predicated scalar loads, so
 // tails and any row stride run the same code.  FFMA2 packs coefficient PAIRS of one pixel.
-// Pass 1 (history): g = X' (y - c) with 2Sum-compensated 32-date blocks, and the Gram
-//   complement Gm = sum over MISSING history dates of x_t x_t^T (x_t x_t^T from a table,
-//   lower triangle); G_v = G_full - Gm is accurate because Gm has few terms, and whole
-//   warps skip dates on which none of their 32 pixels is missing (clustered clouds).
-// Solve: float64 Cholesky of G_v per pixel (in registers), beta' = G_v^-1 g.
+// Pass 1 (history): g = X' (y - c) with 2Sum-compensated 32-date blocks (FFMA2), and the Gram
+//   complement Gm = W X2 on the TENSOR CORES: W[pixel][date] = 1 if missing (exact in tf32),
+//   X2[date][e] = the lower-triangle entries of x_t x_t^T, split hi + lo (tf32 each, ~22 bits).
+//   Every thread writes its pixel's 0/1 row of a 16-date block into its own TMEM lane (the
+//   A operand, tcgen05.st); one thread issues 2 steps x 2 splits of
+//   tcgen05.mma.kind::tf32 (M = 128 pixels, N = p(p+1)/2 padded to 16, K = 8 dates, A from
+//   TMEM, B from shared memory) accumulating Gm in TMEM (lane = pixel), and the x x^T tiles
+//   stream from L2 through a 3-stage shared-memory ring (cp.async.bulk).  G_v = G_full - Gm
+//   is accurate because Gm has few terms; the refinement step below absorbs the rest.
+// Solve: float32 Cholesky of G_v per pixel (in registers), beta' = G_v^-1 g.
 // Pass 2 (history again, L2): two-pass RSS of the valid dates; the last h_v - 1 valid
 //   residuals (and their dates) go to a per-pixel ring (slot 0 = 0: the element before
 //   window 0).  The same sweep accumulates the normal-equation residual e = X_v r, and one
@@ -27,67 +32,177 @@
 //   of p/2 FFMA2 per valid history date; realistic stacks have cond(G_v) < 10.
 // Pass 3 (monitoring): per valid date r, old = ring[s], ring[s] = r, acc += r - old,
 //   crossing |acc| > b_j sigma sqrt(n_v); invalid dates leave the state untouched.
-// The ring is [h][128] floats + [h][128] dates (conflict-free: thread = bank); in shared
-// memory, or in a per-CTA global scratch when h or the x x^T table is too large (BIG).
+// Per-thread scratch, [2h][128] words (thread = bank: conflict-free): the residual ring and
+// the ring dates.  In shared memory, or in a per-CTA global scratch when h or the x x^T table
+// is too large (BIG).
 #pragma once
 
 #include "bwm_common.cuh"
+#include "bwm_kernel_tma.cuh"   // mbarrier / TMEM helpers
 
 namespace bwm {
 
-constexpr int kMaskThreads = 128;       // one pixel per thread
+constexpr int kMaskThreads = 128;       // one pixel per thread; M = 128 of the Gram MMA
 constexpr int kMaskTile = kMaskThreads;
-constexpr int kMaskD = 16;              // dates per register block
+constexpr int kMaskD = 16;              // dates per register block = 2 MMA K-steps
+constexpr int kMaskBStages = 3;         // x x^T tile ring (prefetch distance 2 blocks)
 
 template <int NP>
 struct Gram {
     static constexpr int KK = NP * (NP + 1) / 2;          // lower triangle, (i, j<=i) at i(i+1)/2 + j
-    static constexpr int K2 = (KK + 1) / 2;               // float2 accumulators
-    static constexpr int KP = ((2 * K2 + 3) / 4) * 4;     // padded table row (floats)
+    static constexpr int NN = ((KK + 15) / 16) * 16;      // MMA N (multiple of 16 for M = 128)
+    static constexpr int SB = NN * 128;                   // bytes of one 16-date block: 2 steps x hi/lo
 };
+
+__host__ __device__ constexpr int gram_nn(int p) { return ((p * (p + 1) / 2 + 15) / 16) * 16; }
+__host__ __device__ constexpr int masked_tmem_cols(int p) {
+    return gram_nn(p) + 32 <= 32 ? 32 : gram_nn(p) + 32 <= 64 ? 64 : gram_nn(p) + 32 <= 128 ? 128
+           : gram_nn(p) + 32 <= 256 ? 256 : 512;
+}
+
+// tcgen05 pieces of the Gram MMA -----------------------------------------------------------
+// Shared-memory matrix descriptor, K-major, no swizzle: core matrices of 8 rows x 16 bytes,
+// LBO = byte distance between the two 16-byte K chunks, SBO = between 8-row groups.
+__device__ __forceinline__ uint64_t smem_desc_kmajor(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+    return d;                                  // base offset 0, layout SWIZZLE_NONE
+}
+// Instruction descriptor: D f32, A/B tf32, both K-major, N, M = 128.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+// Per-thread scratch words: ring [h] floats + ring dates [h] uint16.
+__host__ __device__ inline int masked_scratch_words(int h, int p) { return h + (h + 1) / 2 + 0 * p; }
 
 // Shared-memory bytes of the masked kernel (host mirror in bwm_capi.cu).
 __host__ __device__ inline int64_t masked_smem_bytes(int N, int n, int h, int p, bool big) {
     const int sp = (p + 3) & ~3;
-    const int kk = p * (p + 1) / 2, kp = (((kk + 1) / 2 * 2 + 3) / 4) * 4;
-    const int n16 = ((n + kMaskD - 1) / kMaskD) * kMaskD;
-    int64_t bytes = (int64_t)(N + kMaskD) * sp * 4;       // X'^T, zero rows past N
-    if (!big) bytes += (int64_t)n16 * kp * 4 + (int64_t)h * kMaskThreads * 8;
-    return bytes;
+    int64_t bytes = (((int64_t)(N + kMaskD) * sp * 4 + 127) / 128) * 128;   // X'^T, zero rows past N
+    bytes += (int64_t)kMaskBStages * gram_nn(p) * 128;                      // x x^T tile ring
+    if (!big) bytes += (int64_t)masked_scratch_words(h, p) * kMaskThreads * 4;
+    return bytes + (2 * kMaskBStages + 2) * 8 + 16;                         // mbarriers + TMEM slot
+}
+
+// Column J of an in-place float32 Cholesky factorisation of the packed lower triangle L,
+// recursing over J at compile time so every index is a constant (a runtime-indexed register
+// array compiles to select chains: ~1000 instructions at p = 8).
+template <int NP, int J>
+__device__ __forceinline__ void chol_col(float (&L)[NP * (NP + 1) / 2], float (&dinv)[NP], bool& ok) {
+    if constexpr (J < NP) {
+        constexpr int JR = J * (J + 1) / 2;
+        float d = L[JR + J];
+#pragma unroll
+        for (int k = 0; k < J; ++k) d = fmaf(-L[JR + k], L[JR + k], d);
+        ok = ok && d > 1e-6f * fabsf(L[JR + J]);            // numerically singular in float32
+        const float inv = ok ? rsqrtf(d) : 0.f;
+        dinv[J] = inv;
+#pragma unroll
+        for (int i = J + 1; i < NP; ++i) {
+            float sv = L[i * (i + 1) / 2 + J];
+#pragma unroll
+            for (int k = 0; k < J; ++k) sv = fmaf(-L[i * (i + 1) / 2 + k], L[JR + k], sv);
+            L[i * (i + 1) / 2 + J] = sv * inv;
+        }
+        chol_col<NP, J + 1>(L, dinv, ok);
+    }
 }
 
 template <int NP, bool BIG>
 __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
     monitor_kernel_masked(const __grid_constant__ KParams prm) {
     constexpr int SP = Coefs<NP>::SP;
-    constexpr int KK = Gram<NP>::KK, K2 = Gram<NP>::K2, KP = Gram<NP>::KP;
-    constexpr int D = kMaskD;
+    constexpr int KK = Gram<NP>::KK, NN = Gram<NP>::NN, SB = Gram<NP>::SB;
+    constexpr int D = kMaskD, S = kMaskBStages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
     const int n16 = ((n + D - 1) / D) * D;
+    const int nkb = n16 / D;                                           // 16-date blocks of the history
     float* s_x = reinterpret_cast<float*>(smem_raw);                   // [N + D][SP]   X'^T
-    float* s_xx = s_x + (N + D) * SP;                                  // [n16][KP]     x x^T (!BIG)
-    float* s_ring = s_xx + n16 * KP;                                   // [2][h][128]   (!BIG)
-    for (int i = threadIdx.x; i < (N + D) * SP; i += kMaskThreads) s_x[i] = i < N * SP ? prm.xt[i] : 0.f;
-    if (!BIG)
-        for (int i = threadIdx.x; i < n16 * KP; i += kMaskThreads) s_xx[i] = i < n * KP ? prm.xx[i] : 0.f;
+    unsigned char* s_b = smem_raw + (((N + D) * SP * 4 + 127) / 128) * 128;   // [S][SB] x x^T tiles
+    float* s_ring = reinterpret_cast<float*>(s_b + S * SB);           // ring scratch   (!BIG)
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(s_ring) +
+                                                  (BIG ? 0 : masked_scratch_words(h, NP) * kMaskThreads * 4));
+    uint64_t* b_full = s_bar;              // [S]  tile landed
+    uint64_t* b_empty = s_bar + S;         // [S]  MMAs reading the tile are done
+    uint64_t* m_done = s_bar + 2 * S;      // [2]  MMAs reading A buffer b are done
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * S + 2);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (N + D) * SP; i += kMaskThreads) s_x[i] = i < N * SP ? prm.xt[i] : 0.f;
+    if (tid == 0) {
+        for (int i = 0; i < 2 * S + 2; ++i) mbar_init(s_bar + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    constexpr uint32_t kCols = (uint32_t)masked_tmem_cols(NP);
+    if (warp == 0) tmem_alloc(s_tmem, kCols);
+    tmem_fence_before();
     __syncthreads();
-    const float* xx = BIG ? prm.xx : s_xx;      // BIG: the padded table lives in global memory
-    float* ring = (BIG ? prm.ring_g + (int64_t)blockIdx.x * 2 * h * kMaskThreads : s_ring) + threadIdx.x;
-    int* ring_d = reinterpret_cast<int*>(ring + h * kMaskThreads);   // date of each ring entry
+    tmem_fence_after();
+    const uint32_t tbase = *s_tmem;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;            // this warp's TMEM lane quarter
+    const uint32_t d_col = tbase, a_col = tbase + NN;                 // Gm accumulator | 2 x 16 A columns
+    float* ring = (BIG ? prm.ring_g + (int64_t)blockIdx.x * masked_scratch_words(h, NP) * kMaskThreads : s_ring) +
+                  tid;
+    uint16_t* ring_d = reinterpret_cast<uint16_t*>(ring - tid + h * kMaskThreads) + tid;   // ring dates
 
-    const int tid = threadIdx.x;
     const int64_t ld = prm.ld_y;
     const float lam = prm.lambda;
-    const float kE = 2.718281828459045f;
     const int64_t n_tiles = (prm.n_pixels + kMaskTile - 1) / kMaskTile;
+    const int64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t total_blocks = my_tiles * nkb;                      // x x^T tiles this CTA consumes
+
+    // ---- x x^T tile stream (thread 0): block q of the CTA's sequence is history block q % nkb
+    const uint32_t sb_u32 = smem_u32(s_b);
+    auto issue_b = [&](int64_t q) {
+        if (q >= total_blocks) return;
+        const int st = (int)(q % S);
+        bulk_g2s(sb_u32 + st * SB, prm.xx + (q % nkb) * (SB / 4), SB, smem_u32(b_full + st));
+    };
+    if (tid == 0)
+        for (int64_t q = 0; q < S - 1; ++q) issue_b(q);
+    constexpr uint32_t kIdesc = idesc_tf32(NN);
+    int64_t q = 0;                                                     // CTA-wide block counter
 
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int64_t px = tile * kMaskTile + tid;
         const bool act = px < prm.n_pixels;
-        const float* yp = prm.y + (act ? px : 0);
-        auto load = [&](int t, int end) -> float {
-            return (act && t < end) ? __ldg(yp + (int64_t)t * ld) : __int_as_float(0x7fc00000);
+        const float* yp = prm.y + (act ? px : prm.n_pixels - 1);    // idle lanes read a real pixel
+        const float qnan = __int_as_float(0x7fc00000);
+        // D dates from row t0 (rows >= end read as missing); idle lanes see only missing dates
+        // (one predicated path: a full/partial branch here makes the compiler duplicate the
+        // unrolled pass bodies behind it, and the kernel is instruction-fetch bound)
+        auto load = [&](int t0, int end, float (&vb)[D]) {
+            const float* p = yp + (int64_t)t0 * ld;
+            const int rows = act ? end - t0 : 0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                vb[k] = k < rows ? __ldg(p) : qnan;
+                p += ld;
+            }
         };
 
         // ---- pass 0: centre c = first finite value (any finite value would do numerically) -
@@ -97,95 +212,107 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
             if (finitef(v)) { c = v; break; }
         }
 
-        // ---- pass 1: g = X'(y - c) over valid dates; Gm over missing dates ---------------
-        float2 gm[K2], gp[NP / 2], ghi[NP / 2], glo[NP / 2];
-#pragma unroll
-        for (int i = 0; i < K2; ++i) gm[i] = f2(0.f, 0.f);
+        // ---- pass 1: g = X'(y - c) over valid dates (FFMA2); Gm = W X2 on the tensor cores --
+        float2 gp[NP / 2], ghi[NP / 2], glo[NP / 2];
 #pragma unroll
         for (int i = 0; i < NP / 2; ++i) gp[i] = ghi[i] = glo[i] = f2(0.f, 0.f);
         int nv = 0;
-        for (int t0 = 0; t0 < n; t0 += D) {
+        for (int t0 = 0; t0 < n16; t0 += D, ++q) {
             float vb[D];
-#pragma unroll
-            for (int k = 0; k < D; ++k) vb[k] = load(t0 + k, n);
+            load(t0, n, vb);
+            float2 wv[D / 2];                                          // 1 = missing: this block's A row
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 const int t = t0 + k;
                 const bool m = finitef(vb[k]);
                 const float yc = m ? vb[k] - c : 0.f;
                 nv += m ? 1 : 0;
+                if (k & 1) wv[k >> 1].y = m ? 0.f : 1.f; else wv[k >> 1].x = m ? 0.f : 1.f;
                 const float4* x4 = reinterpret_cast<const float4*>(s_x + t * SP);
 #pragma unroll
-                for (int q = 0; q < SP / 4; ++q) {
-                    const float4 x = x4[q];
-                    if (4 * q + 1 < NP) gp[2 * q] = fma2(f2(yc, yc), f2(x.x, x.y), gp[2 * q]);
-                    if (4 * q + 3 < NP) gp[2 * q + 1] = fma2(f2(yc, yc), f2(x.z, x.w), gp[2 * q + 1]);
-                }
-                // rows t >= n carry NaN (missing) but their table rows are zero: no-ops
-                if (__any_sync(0xffffffffu, !m)) {
-                    const float w = m ? 0.f : 1.f;
-                    const float4* r4 = reinterpret_cast<const float4*>(xx + (int64_t)t * KP);
-#pragma unroll
-                    for (int q = 0; q < KP / 4; ++q) {
-                        const float4 a = BIG ? __ldg(r4 + q) : r4[q];
-                        if (2 * q < K2) gm[2 * q] = fma2(f2(w, w), f2(a.x, a.y), gm[2 * q]);
-                        if (2 * q + 1 < K2) gm[2 * q + 1] = fma2(f2(w, w), f2(a.z, a.w), gm[2 * q + 1]);
-                    }
+                for (int qq = 0; qq < SP / 4; ++qq) {
+                    const float4 x = x4[qq];
+                    if (4 * qq + 1 < NP) gp[2 * qq] = fma2(f2(yc, yc), f2(x.x, x.y), gp[2 * qq]);
+                    if (4 * qq + 3 < NP) gp[2 * qq + 1] = fma2(f2(yc, yc), f2(x.z, x.w), gp[2 * qq + 1]);
                 }
             }
             if (((t0 + D) & (kComp - 1)) == 0 || t0 + D >= n) {
 #pragma unroll
                 for (int i = 0; i < NP / 2; ++i) { two_sum(ghi[i], glo[i], gp[i]); gp[i] = f2(0.f, 0.f); }
             }
-        }
-
-        // ---- solve G_v beta' = g in float64 (Cholesky, in registers) --------------------
-        double L[KK];
+            // A buffer q&1 is free once the MMAs of block q-2 completed
+            const int ab = (int)(q & 1);
+            if (q >= 2) mbar_wait(m_done + ab, (uint32_t)(((q >> 1) - 1) & 1));
+            tmem_st16(a_col + lane_off + 16 * ab, wv);
+            tmem_wait_st();
+            tmem_fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                tmem_fence_after();
+                const int st = (int)(q % S);
+                mbar_wait(b_full + st, (uint32_t)((q / S) & 1));
+                const uint32_t bt = sb_u32 + st * SB;
 #pragma unroll
-        for (int i = 0; i < KK; ++i) {
-            const float gmi = (i & 1) ? gm[i >> 1].y : gm[i >> 1].x;
-            L[i] = __ldg(prm.gfull + i) - (double)gmi;
-        }
-        bool ok = nv > NP;
+                for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
-        for (int j = 0; j < NP; ++j) {
-            const int jj = j * (j + 1) / 2 + j;
-            double d = L[jj];
-#pragma unroll
-            for (int k = 0; k < j; ++k) d -= L[j * (j + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
-            ok = ok && d > 1e-9 * fabs(L[jj]) && d > 0.0;
-            const double inv = ok ? rsqrt(d) : 0.0;
-            L[jj] = ok ? d * inv : 1.0;          // L_jj
-#pragma unroll
-            for (int i = j + 1; i < NP; ++i) {
-                double s = L[i * (i + 1) / 2 + j];
-#pragma unroll
-                for (int k = 0; k < j; ++k) s -= L[i * (i + 1) / 2 + k] * L[j * (j + 1) / 2 + k];
-                L[i * (i + 1) / 2 + j] = s * inv;
+                    for (int sp = 0; sp < 2; ++sp)
+                        mma_tf32_ts(d_col, a_col + 16 * ab + 8 * ks,
+                                    smem_desc_kmajor(bt + (2 * ks + sp) * NN * 32, 128, 256), kIdesc,
+                                    (t0 > 0 || ks > 0 || sp > 0) ? 1u : 0u);
+                mma_commit(smem_u32(m_done + ab));
+                mma_commit(smem_u32(b_empty + st));
+                // refill the stage of block q-1 (its MMAs were issued one block ago)
+                if (q >= 1) mbar_wait(b_empty + (int)((q - 1) % S), (uint32_t)(((q - 1) / S) & 1));
+                issue_b(q + S - 1);
             }
         }
-        double z[NP];
+        // the Gram complement of this tile: wait for the last block's MMAs, read this lane
+        mbar_wait(m_done + (int)((q - 1) & 1), (uint32_t)(((q - 1) >> 1) & 1));
+        tmem_fence_after();
+        float gmv[NN];
+#pragma unroll
+        for (int c16 = 0; c16 < NN / 16; ++c16)
+            tmem_ld16(d_col + lane_off + 16 * c16, *reinterpret_cast<float2(*)[8]>(&gmv[16 * c16]));
+        tmem_fence_before();      // the next tile's first MMA overwrites D after a __syncthreads
+
+        // ---- solve G_v beta' = g: float32 Cholesky in registers (G_v formed in float64) -----
+        // Emulated against the float64 oracle: a float32 factor plus the refinement step below
+        // is as accurate as a float64 factor (3e-5 on max |MO| at cond(G_v) = 3e4, 3e-6 at
+        // cond 30), without the float64 register pressure that spilled through the loops.
+        float L[KK], dinv[NP];
+#pragma unroll
+        for (int i = 0; i < KK; ++i) {
+            L[i] = (float)(__ldg(prm.gfull + i) - (double)gmv[i]);
+        }
+        bool ok = nv > NP;
+        chol_col<NP, 0>(L, dinv, ok);
+        // L w = b, L^T x = w  (in place)
+        auto chol_solve = [&](float (&v)[NP]) {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                float sv = v[i];
+#pragma unroll
+                for (int k = 0; k < i; ++k) sv = fmaf(-L[i * (i + 1) / 2 + k], v[k], sv);
+                v[i] = sv * dinv[i];
+            }
+#pragma unroll
+            for (int i = NP - 1; i >= 0; --i) {
+                float sv = v[i];
+#pragma unroll
+                for (int k = i + 1; k < NP; ++k) sv = fmaf(-L[k * (k + 1) / 2 + i], v[k], sv);
+                v[i] = sv * dinv[i];
+            }
+        };
+        float z[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             const float2 gg = ghi[i >> 1], gl = glo[i >> 1];
-            double s = (i & 1) ? (double)gg.y + (double)gl.y : (double)gg.x + (double)gl.x;
-#pragma unroll
-            for (int k = 0; k < i; ++k) s -= L[i * (i + 1) / 2 + k] * z[k];
-            z[i] = s / L[i * (i + 1) / 2 + i];
+            z[i] = (i & 1) ? gg.y + gl.y : gg.x + gl.x;
         }
-#pragma unroll
-        for (int i = NP - 1; i >= 0; --i) {
-            double s = z[i];
-#pragma unroll
-            for (int k = i + 1; k < NP; ++k) s -= L[k * (k + 1) / 2 + i] * z[k];
-            z[i] = s / L[i * (i + 1) / 2 + i];
-        }
+        chol_solve(z);
         float2 nb[NP / 2];    // -beta' in coefficient pairs
 #pragma unroll
-        for (int i = 0; i < NP / 2; ++i) nb[i] = ok ? f2(-(float)z[2 * i], -(float)z[2 * i + 1]) : f2(0.f, 0.f);
-        float Lf[KK];         // the factor, kept (float32) for the refinement step
-#pragma unroll
-        for (int i = 0; i < KK; ++i) Lf[i] = (float)L[i];
+        for (int i = 0; i < NP / 2; ++i) nb[i] = ok ? f2(-z[2 * i], -z[2 * i + 1]) : f2(0.f, 0.f);
         auto resid = [&](float yc, int t) -> float {
             float2 r2 = f2(yc, 0.f);
             const float4* x4 = reinterpret_cast<const float4*>(s_x + t * SP);
@@ -201,7 +328,9 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
         // ---- pass 2: RSS (two-pass) and the history part of window 0 -----------------------
         const int hv = (int)(((int64_t)h * nv) / n);
         const int wfirst = nv - hv + 1;          // 0-based compacted index of window 0's first element
-        int seen = 0, slot = 1;
+        // branch-free bodies: per-pixel state advances by selects, ring writes are predicated
+        constexpr int RS = kMaskThreads;         // ring row stride (words)
+        int seen = 0, so = RS;                   // so: word offset of the next ring slot (slot 1)
         double rss = 0.0;
         float2 e2[NP / 2];                       // X_v r (normal-equation residual)
 #pragma unroll
@@ -209,8 +338,7 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
         if (hv >= 1) ring[0] = 0.f;              // the element before window 0
         for (int t0 = 0; t0 < n; t0 += D) {
             float vb[D];
-#pragma unroll
-            for (int k = 0; k < D; ++k) vb[k] = load(t0 + k, n);
+            load(t0, n, vb);
             float part = 0.f;
 #pragma unroll
             for (int k = 0; k < D; ++k) {
@@ -226,36 +354,39 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
                     if (4 * q + 1 < NP) e2[2 * q] = fma2(f2(rm, rm), f2(x.x, x.y), e2[2 * q]);
                     if (4 * q + 3 < NP) e2[2 * q + 1] = fma2(f2(rm, rm), f2(x.z, x.w), e2[2 * q + 1]);
                 }
-                if (m) {
-                    if (seen >= wfirst) {
-                        ring[slot * kMaskThreads] = r;
-                        ring_d[slot * kMaskThreads] = t;
-                        ++slot;
-                    }
-                    ++seen;
+                const bool inwin = m && seen >= wfirst;
+                if (inwin) {
+                    ring[so] = r;
+                    ring_d[so] = (uint16_t)t;
                 }
+                so += inwin ? RS : 0;
+                seen += m ? 1 : 0;
             }
             rss += (double)part;
         }
+        const int slot = so / RS;
 
         // ---- one refinement step: dbeta = G_v^-1 e; correct RSS and the window residuals ---
         float db[NP];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-            float sv = (i & 1) ? e2[i >> 1].y : e2[i >> 1].x;
+        for (int i = 0; i < NP; ++i) db[i] = (i & 1) ? e2[i >> 1].y : e2[i >> 1].x;
+        double quad = 0.0;                                  // |L^T dbeta|^2 = |w|^2, w = L^-1 e
+        {
 #pragma unroll
-            for (int k = 0; k < i; ++k) sv -= Lf[i * (i + 1) / 2 + k] * db[k];
-            db[i] = sv / Lf[i * (i + 1) / 2 + i];            // L w = e
-        }
-        double quad = 0.0;                                  // |L^T dbeta|^2 = |w|^2
+            for (int i = 0; i < NP; ++i) {
+                float sv = db[i];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) quad += (double)db[i] * (double)db[i];
+                for (int k = 0; k < i; ++k) sv = fmaf(-L[i * (i + 1) / 2 + k], db[k], sv);
+                db[i] = sv * dinv[i];
+                quad += (double)db[i] * (double)db[i];
+            }
 #pragma unroll
-        for (int i = NP - 1; i >= 0; --i) {
-            float sv = db[i];
+            for (int i = NP - 1; i >= 0; --i) {
+                float sv = db[i];
 #pragma unroll
-            for (int k = i + 1; k < NP; ++k) sv -= Lf[k * (k + 1) / 2 + i] * db[k];
-            db[i] = sv / Lf[i * (i + 1) / 2 + i];            // L^T dbeta = w
+                for (int k = i + 1; k < NP; ++k) sv = fmaf(-L[k * (k + 1) / 2 + i], db[k], sv);
+                db[i] = sv * dinv[i];
+            }
         }
         double de = 0.0;
 #pragma unroll
@@ -287,32 +418,38 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
         // ---- pass 3: compacted MOSUM + per-pixel boundary ----------------------------------
         float mx = 0.f, msum = 0.f;
         int first = 0, j = 0;
-        slot = 0;
-        float* const mo_out = prm.mosum;
+        int ro = 0;                              // word offset of the ring slot holding r_{e - h_v}
+        const int ro_end = hv * RS;
+        const float jx0 = (float)(nv + 1) * inv_nv, dx = inv_nv;   // x_j = (n_v + 1 + j) / n_v
+        float* mo_p = prm.mosum ? prm.mosum + px : nullptr;
+        const int64_t ld_out = prm.ld_out;
         for (int t0 = n; t0 < N; t0 += D) {
             float vb[D];
-#pragma unroll
-            for (int k = 0; k < D; ++k) vb[k] = load(t0 + k, N);
+            load(t0, N, vb);
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 const int t = t0 + k;
                 const bool m = finitef(vb[k]) && fit_ok;
                 const float r = resid(m ? vb[k] - c : 0.f, t);
-                if (m) {
-                    const float old = ring[slot * kMaskThreads];
-                    ring[slot * kMaskThreads] = r;
-                    slot = slot + 1 == hv ? 0 : slot + 1;
-                    acc += r - old;
-                    const float x = (float)(nv + 1 + j) * inv_nv;
-                    const float b = lam_sc * sqrtf(__logf(fmaxf(x, kE)));
-                    const float a = fabsf(acc);
-                    mx = fmaxf(mx, a);
-                    if (a > b && first == 0) first = t + 1 - n;
-                    msum += acc;
-                    ++j;
+                const float old = ring[ro];
+                if (m) ring[ro] = r;
+                const int ro1 = ro + RS == ro_end ? 0 : ro + RS;
+                ro = m ? ro1 : ro;
+                acc = m ? acc + (r - old) : acc;
+                // b_j = lambda sqrt(log_plus(x)), log_plus(x) = max(ln x, 1): branch-free, exactly
+                // lambda while x <= e (rsqrt(1) = 1); elsewhere within ~1e-7 of the float64 value
+                const float x = fmaf((float)j, dx, jx0);
+                const float lp = fmaxf(__log2f(x) * 0.69314718f, 1.f);
+                const float b = lam_sc * (lp * rsqrtf(lp));
+                const float a = fabsf(acc);
+                mx = m ? fmaxf(mx, a) : mx;
+                first = (m && a > b && first == 0) ? t + 1 - n : first;
+                msum += m ? acc : 0.f;
+                j += m ? 1 : 0;
+                if (mo_p) {
+                    if (act && t < N) *mo_p = m ? acc * inv : __int_as_float(0x7fc00000);
+                    mo_p += ld_out;
                 }
-                if (mo_out && act && t < N)
-                    mo_out[(int64_t)(t - n) * prm.ld_out + px] = m ? acc * inv : __int_as_float(0x7fc00000);
             }
         }
 
@@ -336,6 +473,10 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
             }
         }
     }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(tbase, kCols);
 }
 
 }  // namespace bwm
