@@ -28,7 +28,7 @@ BWM_DECLARE_PICK(12)
 BWM_DECLARE_PICK(14)
 BWM_DECLARE_PICK(16)
 BWM_DECLARE_PICK(18)
-#define BWM_DECLARE_PICK_MASKED(NP) bwm::KernelFn bwm_pick_masked_p##NP(int big);
+#define BWM_DECLARE_PICK_MASKED(NP) bwm::KernelFn bwm_pick_masked_p##NP(int big, int keep);
 BWM_DECLARE_PICK_MASKED(4)
 BWM_DECLARE_PICK_MASKED(6)
 BWM_DECLARE_PICK_MASKED(8)
@@ -171,16 +171,16 @@ KernelFn pick(int p, Kind kind, int mode) {
     }
 }
 
-KernelFn pick_masked(int p, bool big) {
+KernelFn pick_masked(int p, bool big, bool keep) {
     switch (p) {
-        case 4: return bwm_pick_masked_p4(big);
-        case 6: return bwm_pick_masked_p6(big);
-        case 8: return bwm_pick_masked_p8(big);
-        case 10: return bwm_pick_masked_p10(big);
-        case 12: return bwm_pick_masked_p12(big);
-        case 14: return bwm_pick_masked_p14(big);
-        case 16: return bwm_pick_masked_p16(big);
-        case 18: return bwm_pick_masked_p18(big);
+        case 4: return bwm_pick_masked_p4(big, keep);
+        case 6: return bwm_pick_masked_p6(big, keep);
+        case 8: return bwm_pick_masked_p8(big, keep);
+        case 10: return bwm_pick_masked_p10(big, keep);
+        case 12: return bwm_pick_masked_p12(big, keep);
+        case 14: return bwm_pick_masked_p14(big, keep);
+        case 16: return bwm_pick_masked_p16(big, keep);
+        case 18: return bwm_pick_masked_p18(big, keep);
         default: return nullptr;
     }
 }
@@ -360,10 +360,11 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
     if ((e = cudaMemcpy(plan->d_gfull, gf.data(), gf.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
     plan->lambda = (float)tb->bound[0];    // bound_0 = crit * sqrt(log_plus((n+1)/n)) = crit
-    KernelFn fn = pick_masked(p, plan->mbig);
-    if ((e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin)) !=
-        cudaSuccess)
-        return fail(e, "cudaFuncSetAttribute");
+    KernelFn fn = pick_masked(p, plan->mbig, false);
+    for (int keep = 0; keep < 2; ++keep)
+        if ((e = cudaFuncSetAttribute((const void*)pick_masked(p, plan->mbig, keep), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      max_optin)) != cudaSuccess)
+            return fail(e, "cudaFuncSetAttribute");
     plan->bpm_masked = resident_ctas((const void*)fn, bwm::kMaskThreads, plan->smem_masked,
                                      bwm::masked_tmem_cols(p), plan->device, &e);
     if (e != cudaSuccess) return fail(e, "cudaFuncGetAttributes");
@@ -637,7 +638,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         k.lambda = plan->lambda;
         const int64_t tiles = (n_pixels + bwm::kMaskTile - 1) / bwm::kMaskTile;
         const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * plan->bpm_masked);
-        pick_masked(d.n_params, plan->mbig)<<<(unsigned)grid, bwm::kMaskThreads, (size_t)plan->smem_masked, st>>>(k);
+        pick_masked(d.n_params, plan->mbig, out->mosum != nullptr)<<<(unsigned)grid, bwm::kMaskThreads, (size_t)plan->smem_masked, st>>>(k);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
         ++launched;

@@ -45,7 +45,8 @@ namespace bwm {
 constexpr int kMaskThreads = 128;       // one pixel per thread; M = 128 of the Gram MMA
 constexpr int kMaskTile = kMaskThreads;
 constexpr int kMaskD = 16;              // dates per register block = 2 MMA K-steps
-constexpr int kMaskBStages = 3;         // x x^T tile ring (prefetch distance 2 blocks)
+constexpr int kMaskBStages = 4;         // x x^T tile ring: refilled 2 blocks behind, 2 ahead
+constexpr int kMaskABufs = 4;           // TMEM A buffers (16 columns each)
 
 template <int NP>
 struct Gram {
@@ -56,8 +57,8 @@ struct Gram {
 
 __host__ __device__ constexpr int gram_nn(int p) { return ((p * (p + 1) / 2 + 15) / 16) * 16; }
 __host__ __device__ constexpr int masked_tmem_cols(int p) {
-    return gram_nn(p) + 32 <= 32 ? 32 : gram_nn(p) + 32 <= 64 ? 64 : gram_nn(p) + 32 <= 128 ? 128
-           : gram_nn(p) + 32 <= 256 ? 256 : 512;
+    return gram_nn(p) + 16 * kMaskABufs <= 64 ? 64 : gram_nn(p) + 16 * kMaskABufs <= 128 ? 128
+           : gram_nn(p) + 16 * kMaskABufs <= 256 ? 256 : 512;
 }
 
 // tcgen05 pieces of the Gram MMA -----------------------------------------------------------
@@ -105,7 +106,7 @@ __host__ __device__ inline int64_t masked_smem_bytes(int N, int n, int h, int p,
     int64_t bytes = (((int64_t)(N + kMaskD) * sp * 4 + 127) / 128) * 128;   // X'^T, zero rows past N
     bytes += (int64_t)kMaskBStages * gram_nn(p) * 128;                      // x x^T tile ring
     if (!big) bytes += (int64_t)masked_scratch_words(h, p) * kMaskThreads * 4;
-    return bytes + (2 * kMaskBStages + 2) * 8 + 16;                         // mbarriers + TMEM slot
+    return bytes + (2 * kMaskBStages + kMaskABufs) * 8 + 16;                // mbarriers + TMEM slot
 }
 
 // Column J of an in-place float32 Cholesky factorisation of the packed lower triangle L,
@@ -132,12 +133,15 @@ __device__ __forceinline__ void chol_col(float (&L)[NP * (NP + 1) / 2], float (&
     }
 }
 
-template <int NP, bool BIG>
+// idle lanes of a tail tile read this NaN (stride 0): every date missing, no per-row test
+static __device__ const unsigned int kNanRow[1] = {0x7fc00000u};
+
+template <int NP, bool BIG, bool KEEP>
 __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
     monitor_kernel_masked(const __grid_constant__ KParams prm) {
     constexpr int SP = Coefs<NP>::SP;
     constexpr int KK = Gram<NP>::KK, NN = Gram<NP>::NN, SB = Gram<NP>::SB;
-    constexpr int D = kMaskD, S = kMaskBStages;
+    constexpr int D = kMaskD, S = kMaskBStages, AB = kMaskABufs;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
     const int n16 = ((n + D - 1) / D) * D;
@@ -149,12 +153,12 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
                                                   (BIG ? 0 : masked_scratch_words(h, NP) * kMaskThreads * 4));
     uint64_t* b_full = s_bar;              // [S]  tile landed
     uint64_t* b_empty = s_bar + S;         // [S]  MMAs reading the tile are done
-    uint64_t* m_done = s_bar + 2 * S;      // [2]  MMAs reading A buffer b are done
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * S + 2);
+    uint64_t* m_done = s_bar + 2 * S;      // [AB] MMAs reading A buffer b are done
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * S + AB);
     const int tid = threadIdx.x, warp = tid >> 5;
     for (int i = tid; i < (N + D) * SP; i += kMaskThreads) s_x[i] = i < N * SP ? prm.xt[i] : 0.f;
     if (tid == 0) {
-        for (int i = 0; i < 2 * S + 2; ++i) mbar_init(s_bar + i, 1);
+        for (int i = 0; i < 2 * S + AB; ++i) mbar_init(s_bar + i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     constexpr uint32_t kCols = (uint32_t)masked_tmem_cols(NP);
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
     tmem_fence_after();
     const uint32_t tbase = *s_tmem;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;            // this warp's TMEM lane quarter
-    const uint32_t d_col = tbase, a_col = tbase + NN;                 // Gm accumulator | 2 x 16 A columns
+    const uint32_t d_col = tbase, a_col = tbase + NN;                 // Gm accumulator | AB x 16 A columns
     float* ring = (BIG ? prm.ring_g + (int64_t)blockIdx.x * masked_scratch_words(h, NP) * kMaskThreads : s_ring) +
                   tid;
     uint16_t* ring_d = reinterpret_cast<uint16_t*>(ring - tid + h * kMaskThreads) + tid;   // ring dates
@@ -183,34 +187,33 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
         bulk_g2s(sb_u32 + st * SB, prm.xx + (q % nkb) * (SB / 4), SB, smem_u32(b_full + st));
     };
     if (tid == 0)
-        for (int64_t q = 0; q < S - 1; ++q) issue_b(q);
+        for (int64_t q = 0; q < S - 2; ++q) issue_b(q);
     constexpr uint32_t kIdesc = idesc_tf32(NN);
     int64_t q = 0;                                                     // CTA-wide block counter
 
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int64_t px = tile * kMaskTile + tid;
         const bool act = px < prm.n_pixels;
-        const float* yp = prm.y + (act ? px : prm.n_pixels - 1);    // idle lanes read a real pixel
+        const float* yp = act ? prm.y + px : reinterpret_cast<const float*>(kNanRow);
+        const int64_t ldl = act ? ld : 0;
         const float qnan = __int_as_float(0x7fc00000);
-        // D dates from row t0 (rows >= end read as missing); idle lanes see only missing dates
-        // (one predicated path: a full/partial branch here makes the compiler duplicate the
-        // unrolled pass bodies behind it, and the kernel is instruction-fetch bound)
+        // D dates from row t0; rows >= end read as missing (only the last block of a pass)
         auto load = [&](int t0, int end, float (&vb)[D]) {
-            const float* p = yp + (int64_t)t0 * ld;
-            const int rows = act ? end - t0 : 0;
+            const float* p = yp + (int64_t)t0 * ldl;
+            if (t0 + D <= end) {
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
-                vb[k] = k < rows ? __ldg(p) : qnan;
-                p += ld;
+                for (int k = 0; k < D; ++k) vb[k] = __ldg(p + k * ldl);
+            } else {
+#pragma unroll
+                for (int k = 0; k < D; ++k) vb[k] = t0 + k < end ? __ldg(p + k * ldl) : qnan;
             }
         };
 
-        // ---- pass 0: centre c = first finite value (any finite value would do numerically) -
+        // centre c: the first finite history value, taken on the fly in pass 1 (any finite value
+        // would do numerically; dates before it are missing and contribute nothing).  A pixel
+        // with no finite history value is invalid (n_v = 0) and keeps c = 0.
         float c = 0.f;
-        for (int t = 0; t < N && act; ++t) {
-            const float v = __ldg(yp + (int64_t)t * ld);
-            if (finitef(v)) { c = v; break; }
-        }
+        bool have_c = false;
 
         // ---- pass 1: g = X'(y - c) over valid dates (FFMA2); Gm = W X2 on the tensor cores --
         float2 gp[NP / 2], ghi[NP / 2], glo[NP / 2];
@@ -225,6 +228,8 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
             for (int k = 0; k < D; ++k) {
                 const int t = t0 + k;
                 const bool m = finitef(vb[k]);
+                c = (m && !have_c) ? vb[k] : c;
+                have_c = have_c || m;
                 const float yc = m ? vb[k] - c : 0.f;
                 nv += m ? 1 : 0;
                 if (k & 1) wv[k >> 1].y = m ? 0.f : 1.f; else wv[k >> 1].x = m ? 0.f : 1.f;
@@ -241,8 +246,8 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
                 for (int i = 0; i < NP / 2; ++i) { two_sum(ghi[i], glo[i], gp[i]); gp[i] = f2(0.f, 0.f); }
             }
             // A buffer q&1 is free once the MMAs of block q-2 completed
-            const int ab = (int)(q & 1);
-            if (q >= 2) mbar_wait(m_done + ab, (uint32_t)(((q >> 1) - 1) & 1));
+            const int ab = (int)(q % AB);
+            if (q >= AB) mbar_wait(m_done + ab, (uint32_t)((q / AB - 1) & 1));
             tmem_st16(a_col + lane_off + 16 * ab, wv);
             tmem_wait_st();
             tmem_fence_before();
@@ -261,13 +266,13 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
                                     (t0 > 0 || ks > 0 || sp > 0) ? 1u : 0u);
                 mma_commit(smem_u32(m_done + ab));
                 mma_commit(smem_u32(b_empty + st));
-                // refill the stage of block q-1 (its MMAs were issued one block ago)
-                if (q >= 1) mbar_wait(b_empty + (int)((q - 1) % S), (uint32_t)(((q - 1) / S) & 1));
-                issue_b(q + S - 1);
+                // refill the stage of block q-2 (its MMAs were issued two blocks ago) with block q+2
+                if (q >= 2) mbar_wait(b_empty + (int)((q - 2) % S), (uint32_t)(((q - 2) / S) & 1));
+                issue_b(q + S - 2);
             }
         }
         // the Gram complement of this tile: wait for the last block's MMAs, read this lane
-        mbar_wait(m_done + (int)((q - 1) & 1), (uint32_t)(((q - 1) >> 1) & 1));
+        mbar_wait(m_done + (int)((q - 1) % AB), (uint32_t)(((q - 1) / AB) & 1));
         tmem_fence_after();
         float gmv[NN];
 #pragma unroll
@@ -421,11 +426,14 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
         int ro = 0;                              // word offset of the ring slot holding r_{e - h_v}
         const int ro_end = hv * RS;
         const float jx0 = (float)(nv + 1) * inv_nv, dx = inv_nv;   // x_j = (n_v + 1 + j) / n_v
-        float* mo_p = prm.mosum ? prm.mosum + px : nullptr;
+        float* mo_p = KEEP ? prm.mosum + px : nullptr;
         const int64_t ld_out = prm.ld_out;
+        // log_plus(x) = 1 while x = (n_v + 1 + j) / n_v <= e, i.e. j < je: b_j = lambda exactly
+        const int je = fit_ok ? (int)floorf(1.718281828f * (float)nv - 1.f) + 1 : 0x3fffffff;
         for (int t0 = n; t0 < N; t0 += D) {
             float vb[D];
             load(t0, N, vb);
+            const bool slow = __any_sync(0xffffffffu, j + D > je);   // warp-uniform
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 const int t = t0 + k;
@@ -438,16 +446,19 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
                 acc = m ? acc + (r - old) : acc;
                 // b_j = lambda sqrt(log_plus(x)), log_plus(x) = max(ln x, 1): branch-free, exactly
                 // lambda while x <= e (rsqrt(1) = 1); elsewhere within ~1e-7 of the float64 value
-                const float x = fmaf((float)j, dx, jx0);
-                const float lp = fmaxf(__log2f(x) * 0.69314718f, 1.f);
-                const float b = lam_sc * (lp * rsqrtf(lp));
+                float b = lam_sc;
+                if (slow) {
+                    const float x = fmaf((float)j, dx, jx0);
+                    const float lp = fmaxf(__log2f(x) * 0.69314718f, 1.f);
+                    b = lam_sc * (lp * rsqrtf(lp));
+                }
                 const float a = fabsf(acc);
                 mx = m ? fmaxf(mx, a) : mx;
                 first = (m && a > b && first == 0) ? t + 1 - n : first;
                 msum += m ? acc : 0.f;
                 j += m ? 1 : 0;
-                if (mo_p) {
-                    if (act && t < N) *mo_p = m ? acc * inv : __int_as_float(0x7fc00000);
+                if (KEEP) {
+                    if (act && t < N) *mo_p = m ? acc * inv : qnan;
                     mo_p += ld_out;
                 }
             }

@@ -26,9 +26,11 @@ using KernelFn = void (*)(const KParams);
         }                                                                                        \
     }
 
-// Defines bwm::KernelFn bwm_pick_masked_p<NP>(int big): the masked-NaN kernel with its x x^T
-// table and residual rings in shared memory (big = 0) or global memory (big = 1).
+// Defines bwm::KernelFn bwm_pick_masked_p<NP>(int big, int keep): the masked-NaN kernel with
+// its residual rings in shared memory (big = 0) or global memory (big = 1), writing the MOSUM
+// matrix (keep = 1) or not.
 #define BWM_DEFINE_PICK_MASKED(NP)                                                               \
-    bwm::KernelFn bwm_pick_masked_p##NP(int big) {                                               \
-        return big ? bwm::monitor_kernel_masked<NP, true> : bwm::monitor_kernel_masked<NP, false>; \
+    bwm::KernelFn bwm_pick_masked_p##NP(int big, int keep) {                                     \
+        if (keep) return big ? bwm::monitor_kernel_masked<NP, true, true> : bwm::monitor_kernel_masked<NP, false, true>; \
+        return big ? bwm::monitor_kernel_masked<NP, true, false> : bwm::monitor_kernel_masked<NP, false, false>;         \
     }
