@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BWM_ABI_VERSION 4
+#define BWM_ABI_VERSION 5
 
 /* error codes (negative); positive returns are cudaError_t values */
 #define BWM_OK 0
@@ -47,6 +47,8 @@ extern "C" {
 #define BWM_E_SMEM (-4)        /* tables + MOSUM ring exceed shared memory      */
 #define BWM_E_DEVICE (-5)      /* plan used on a different device               */
 #define BWM_E_ZERO_SIGMA (-6)  /* not returned by bwm_monitor; see zero_sigma   */
+#define BWM_E_IO (-7)          /* file cannot be opened / read / written        */
+#define BWM_E_FORMAT (-8)      /* file shorter than the payload it declares     */
 
 /* Geometry shared by every pixel of a batch (reference MonitorConfig, engine.py:102-134). */
 typedef struct bwm_dims {
@@ -134,6 +136,36 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
  */
 int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t n_pixels,
                      int64_t pixel_offset, const bwm_outputs* out_host);
+
+/*
+ * End-to-end call from a BTS1 stack FILE (reference dataio.read_stack, dataio.py:79-115,
+ * followed by monitor_batch): the time-major float32 payload of n_pixels columns and
+ * dims.n_obs rows starts at byte payload_offset (after the header and optional axis, which
+ * the caller parsed — the plan's time axis comes from it).  io_threads threads pread row
+ * blocks of the payload into pinned staging slots while earlier blocks are copied to HBM, so
+ * the file read, the PCIe transfer and (for stacks larger than device memory) the kernel
+ * overlap.  io_threads < 1: min(8, hardware threads).  Outputs as for bwm_monitor_host.
+ * Returns BWM_E_IO / BWM_E_FORMAT for unreadable or truncated files.
+ */
+int bwm_monitor_file(bwm_plan* plan, const char* path, int64_t payload_offset, int64_t n_pixels,
+                     int io_threads, const bwm_outputs* out_host);
+
+/*
+ * Parallel read of a time-major float32 payload [n_obs][n_pixels] at byte `offset` of a file
+ * into dst (any host memory; pinned makes the later H2D faster).  The read half of
+ * dataio.read_stack (dataio.py:110-114).  threads < 1: all hardware threads.
+ */
+int bwm_read_payload(const char* path, int64_t offset, int64_t n_obs, int64_t n_pixels, float* dst,
+                     int threads);
+
+/*
+ * Break-map CSV (reference dataio.write_break_map, dataio.py:168-182), byte-identical:
+ * header "pixel,valid,detected,first_break,max_abs_mo", one row per pixel in order,
+ * first_break empty when 0, max_abs_mo at 9 significant digits.  Rows are formatted by
+ * `threads` threads (< 1: all).  Returns the row count or a negative BWM_E_* code.
+ */
+int64_t bwm_write_break_map(const char* path, int64_t n_pixels, const uint8_t* valid, const uint8_t* detected,
+                            const int64_t* first_break, const double* max_abs_mo, int threads);
 
 /* Kernel time (ms) of the last bwm_monitor_host call, summed over chunks; and its
    H2D/D2H byte counts.  For PhaseTimings. */

@@ -19,13 +19,15 @@ BWM_E_DIMS = -2
 BWM_E_PARAMS = -3
 BWM_E_SMEM = -4
 BWM_E_DEVICE = -5
+BWM_E_IO = -7
+BWM_E_FORMAT = -8
 
 BWM_NAN_FILL = 0
 BWM_NAN_MASK = 1
 NAN_MODES = {"fill": BWM_NAN_FILL, "mask": BWM_NAN_MASK}
 
 INT64_MAX = (1 << 63) - 1
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 class Dims(C.Structure):
@@ -81,6 +83,11 @@ SIGNATURES = [
      [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Outputs), C.c_void_p]),
     ("bwm_monitor_host", C.c_int,
      [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Outputs)]),
+    ("bwm_monitor_file", C.c_int,
+     [C.c_void_p, C.c_char_p, C.c_int64, C.c_int64, C.c_int, C.POINTER(Outputs)]),
+    ("bwm_read_payload", C.c_int, [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int]),
+    ("bwm_write_break_map", C.c_int64,
+     [C.c_char_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     ("bwm_last_host_stats", C.c_int,
      [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("bwm_plan_info", C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
@@ -128,6 +135,12 @@ def check(rc: int, what: str) -> None:
     msg = f"{what}: {last_error()}"
     if rc in (BWM_E_DIMS, BWM_E_NULL, BWM_E_PARAMS):
         raise ValueError(msg)
+    if rc == BWM_E_IO:
+        raise OSError(msg)
+    if rc == BWM_E_FORMAT:
+        from .errors import StackFormatError
+
+        raise StackFormatError(last_error())
     raise DeviceError(msg)
 
 

@@ -5,6 +5,7 @@
 // host-buffer pipeline (bwm_monitor_host) that streams pixel chunks through the GPU
 // with H2D / kernel / D2H overlapped on separate streams.
 #include "../../include/bwm.h"
+#include "bwm_io.h"
 #include "bwm_variants.cuh"
 
 #include <atomic>
@@ -14,7 +15,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -58,6 +62,17 @@ int set_err(int code, const char* fmt, ...) {
     g_err = buf;
     return code;
 }
+
+}  // namespace
+
+namespace bwm {
+int set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+}  // namespace bwm
+
+namespace {
 
 #define BWM_CUDA(call)                                                                  \
     do {                                                                                \
@@ -241,6 +256,7 @@ struct bwm_plan {
     double* d_gfull = nullptr;
     float* d_ring = nullptr;           // [sms * bpm_masked][h][128] when mbig
     HostPipe pipe;
+    std::unique_ptr<bwm::StagedReader> freader;   // bwm_monitor_file: pinned slots + reader pool
     std::mutex mu;                     // serialises bwm_monitor_host on one plan
 };
 
@@ -745,10 +761,13 @@ static int pipe_ensure(bwm_plan* plan, int64_t chunk, int nbuf, const PipeNeeds&
     return BWM_OK;
 }
 
-int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t n_pixels,
-                     int64_t pixel_offset, const bwm_outputs* out) {
+// The host pipeline behind bwm_monitor_host (source: host memory y_host, row stride ld_y)
+// and bwm_monitor_file (source: a time-major payload file; rectangles are read into pinned
+// slots by a thread pool while earlier rectangles are copied to HBM).
+static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, const bwm::PayloadFile* file,
+                            int io_threads, int64_t n_pixels, int64_t pixel_offset, const bwm_outputs* out) {
     if (!plan) return set_err(BWM_E_NULL, "plan is NULL");
-    if (!y_host || !out || !out->valid || !out->zero_sigma_pixel || !(out->first_idx || out->first_break) ||
+    if (!(y_host || file) || !out || !out->valid || !out->zero_sigma_pixel || !(out->first_idx || out->first_break) ||
         !(out->max_abs || out->max_abs_f64))
         return set_err(BWM_E_NULL,
                        "y, valid, zero_sigma_pixel, first_idx|first_break and max_abs|max_abs_f64 are required");
@@ -772,7 +791,12 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
     const int64_t whole = ((n_pixels + bwm::kTile - 1) / bwm::kTile) * bwm::kTile;
     int64_t chunk;
     int nbuf;
-    if (pipe_bytes(d, whole, 1, need) + (512ull << 20) <= avail) {
+    const char* force_chunk = std::getenv("BWM_HOST_CHUNK");       // tests: exercise the chunked pipeline
+    const int64_t forced = force_chunk ? ((std::atoll(force_chunk) + bwm::kTile - 1) / bwm::kTile) * bwm::kTile : 0;
+    if (forced > 0 && forced < whole) {
+        chunk = forced;
+        nbuf = 2;
+    } else if (pipe_bytes(d, whole, 1, need) + (512ull << 20) <= avail) {
         chunk = whole;
         nbuf = 1;
     } else {
@@ -794,6 +818,36 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
     BWM_CUDA(cudaStreamWaitEvent(hp.s_h2d[1], t_start, 0));
 
     const int64_t n_chunks = (n_pixels + chunk - 1) / chunk;
+    std::vector<bwm::Rect> rects;
+    std::vector<int64_t> rect_begin(1, 0);
+    std::vector<cudaEvent_t> slot_ev;
+    std::deque<int64_t> pending;
+    int K = 0;
+    if (!plan->freader) plan->freader.reset(new bwm::StagedReader());
+    bwm::StagedReader& reader = *plan->freader;
+    if (file) {
+        const char* slot_env = std::getenv("BWM_IO_SLOT_BYTES");     // tests: small slots split rows
+        const int64_t slot_bytes = slot_env ? std::max<int64_t>(256, std::atoll(slot_env)) : (32ll << 20);
+        for (int64_t c = 0; c < n_chunks; ++c) {
+            bwm::plan_rects(N, c * chunk, std::min(n_pixels, (c + 1) * chunk), c, slot_bytes, &rects);
+            rect_begin.push_back((int64_t)rects.size());
+        }
+        const int threads = std::max(1, io_threads);
+        K = std::max(4, std::min(threads + 4, 24));
+        std::string err;
+        if (int e = reader.ensure(K, slot_bytes, &err)) return set_err(e, "%s", err.c_str());
+        slot_ev.resize((size_t)K, nullptr);
+        for (auto& ev : slot_ev) BWM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        reader.start(file, &rects, threads);
+    }
+    struct ReaderGuard {        // joins the reader threads and frees the slot events on every exit
+        bwm::StagedReader& r;
+        std::vector<cudaEvent_t>& ev;
+        ~ReaderGuard() {
+            r.stop();
+            for (auto& e : ev) if (e) cudaEventDestroy(e);
+        }
+    } reader_guard{reader, slot_ev};
     int64_t h2d = 0, d2h = 0;
     std::vector<cudaEvent_t> kev((size_t)(2 * n_chunks), nullptr);   // per-chunk kernel timing
     for (auto& ev : kev) BWM_CUDA(cudaEventCreate(&ev));
@@ -804,7 +858,30 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
         cudaStream_t sh = hp.s_h2d[b], s = hp.s_k[b];
         // buffer b is free once chunk c-nbuf finished its D2H
         if (c >= nbuf) BWM_CUDA(cudaStreamWaitEvent(sh, hp.ev_free[b], 0));
-        if (ld_y == w) {
+        if (file) {
+            // rectangles of this chunk, alternating over the two copy engines in whole-stack mode
+            for (int64_t g = rect_begin[(size_t)c]; g < rect_begin[(size_t)c + 1]; ++g) {
+                const bwm::Rect& r = rects[(size_t)g];
+                const float* src = reader.wait(g);
+                if (!src) return set_err(BWM_E_IO, "%s", reader.error().c_str());
+                cudaStream_t cs = nbuf == 1 ? hp.s_h2d[g & 1] : sh;
+                const int64_t rw = r.c1 - r.c0;
+                BWM_CUDA(cudaMemcpy2DAsync(hp.d_y[b] + r.r0 * w + (r.c0 - p0), (size_t)w * 4, src, (size_t)rw * 4,
+                                           (size_t)rw * 4, (size_t)(r.r1 - r.r0), cudaMemcpyHostToDevice, cs));
+                BWM_CUDA(cudaEventRecord(slot_ev[(size_t)(g % K)], cs));
+                pending.push_back(g);
+                while ((int)pending.size() > K / 2) {           // refill the oldest slots
+                    const int64_t o = pending.front();
+                    BWM_CUDA(cudaEventSynchronize(slot_ev[(size_t)(o % K)]));
+                    reader.release(o);
+                    pending.pop_front();
+                }
+            }
+            if (nbuf == 1) {
+                BWM_CUDA(cudaEventRecord(hp.ev_in[1], hp.s_h2d[1]));
+                BWM_CUDA(cudaStreamWaitEvent(s, hp.ev_in[1], 0));
+            }
+        } else if (ld_y == w) {
             // contiguous block: split in two halves on both copy streams (one engine each)
             const size_t total = (size_t)w * 4 * N, half = (total / 2) & ~(size_t)255;
             BWM_CUDA(cudaMemcpyAsync(hp.d_y[b], y_host + p0, half, cudaMemcpyHostToDevice, sh));
@@ -874,6 +951,10 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
         kernel_ms += ms;
     }
     for (auto& ev : kev) cudaEventDestroy(ev);
+    for (int64_t g : pending) {
+        BWM_CUDA(cudaEventSynchronize(slot_ev[(size_t)(g % K)]));
+        reader.release(g);
+    }
     for (int b = 0; b < 2; ++b) {
         BWM_CUDA(cudaStreamSynchronize(hp.s_k[b]));
         BWM_CUDA(cudaStreamSynchronize(hp.s_h2d[b]));
@@ -894,6 +975,23 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
     hp.last_h2d = h2d;
     hp.last_d2h = d2h;
     return BWM_OK;
+}
+
+int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t n_pixels,
+                     int64_t pixel_offset, const bwm_outputs* out_host) {
+    return monitor_pipeline(plan, y_host, ld_y, nullptr, 0, n_pixels, pixel_offset, out_host);
+}
+
+int bwm_monitor_file(bwm_plan* plan, const char* path, int64_t payload_offset, int64_t n_pixels,
+                     int io_threads, const bwm_outputs* out_host) {
+    if (!plan) return set_err(BWM_E_NULL, "plan is NULL");
+    if (!path) return set_err(BWM_E_NULL, "path is NULL");
+    if (n_pixels < 1) return set_err(BWM_E_DIMS, "stack needs at least one pixel");
+    bwm::PayloadFile f;
+    std::string err;
+    if (int rc = f.open(path, payload_offset, plan->dims.n_obs, n_pixels, &err)) return set_err(rc, "%s", err.c_str());
+    if (io_threads < 1) io_threads = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency()));
+    return monitor_pipeline(plan, nullptr, n_pixels, &f, io_threads, n_pixels, 0, out_host);
 }
 
 int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import hashlib
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -212,6 +213,22 @@ class DevicePlan:
         if y.shape[0] != self.n_obs:
             raise ValueError(f"expected y of shape ({self.n_obs}, P), got {y.shape}")
         P = int(y.shape[1])
+        call = lambda o: self._lib.bwm_monitor_host(self._handle, y.ctypes.data, y.strides[0] // 4, P,  # noqa: E731
+                                                    int(pixel_offset), o)
+        return self._host_call(call, "bwm_monitor_host", P, keep_mosum, beta, mean, ref_dtypes)
+
+    def run_file(self, path, payload_offset: int, n_pixels: int, *, keep_mosum: bool = False, beta: bool = False,
+                 mean: bool = False, io_threads: int = 0, ref_dtypes: bool = True) -> DeviceResult:
+        """Monitor the time-major payload of a BTS1 file (dataio.py:1-13) straight from disk:
+        libbwm reads row blocks into pinned slots on io_threads threads while earlier blocks
+        are copied to HBM (bwm_monitor_file)."""
+        P = int(n_pixels)
+        raw = os.fsencode(path)
+        call = lambda o: self._lib.bwm_monitor_file(self._handle, raw, int(payload_offset), P,  # noqa: E731
+                                                    int(io_threads), o)
+        return self._host_call(call, "bwm_monitor_file", P, keep_mosum, beta, mean, ref_dtypes)
+
+    def _host_call(self, call, what, P, keep_mosum, beta, mean, ref_dtypes) -> DeviceResult:
         out = DeviceResult(
             valid=_pinned(P, np.uint8),
             first_idx=None if ref_dtypes else _pinned(P, np.int32),
@@ -230,8 +247,7 @@ class DevicePlan:
                          ptr(out.mo_mean), ptr(out.mosum), P, zero.ctypes.data,
                          ptr(out.first_break), ptr(out.max_abs_f64), ptr(out.detected))
         t0 = time.perf_counter()
-        _lib.check(self._lib.bwm_monitor_host(self._handle, y.ctypes.data, y.strides[0] // 4, P,
-                                              int(pixel_offset), C.byref(o)), "bwm_monitor_host")
+        _lib.check(call(C.byref(o)), what)
         out.total_ms = (time.perf_counter() - t0) * 1e3
         k_ms, tot, h2d, d2h = C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
         self._lib.bwm_last_host_stats(self._handle, C.byref(k_ms), C.byref(tot), C.byref(h2d), C.byref(d2h))

@@ -243,7 +243,10 @@ def profile_run(stack: SeriesStack, config: MonitorConfig, threads: Optional[int
     return _run(stack, config, threads, block_size, False, False, False, device)
 
 
-def _run(stack, config, threads, block_size, keep_mosum, return_beta, return_mean, device):
+def _run(stack, config, threads, block_size, keep_mosum, return_beta, return_mean, device, source=None):
+    """One batch through the GPU.  `source` = (path, payload_offset) monitors a BTS1 file's
+    payload directly (dataio.monitor_file); `stack` then only needs n_obs, n_pixels and the
+    time axis."""
     clock = time.perf_counter
     started = clock()
     if config.history >= stack.n_obs:
@@ -256,14 +259,14 @@ def _run(stack, config, threads, block_size, keep_mosum, return_beta, return_mea
     mark = clock()
     design = build_design_matrix(stack.time_axis, config.freq, config.harmonics)
     fit_mapping(design, config.history)        # the reference's error contract (model.py:118-152)
-    if _is_cuda_tensor(stack.data) and device is None:
+    on_device = source is None and _is_cuda_tensor(stack.data)
+    if on_device and device is None:
         device = stack.data.device
     plan = DevicePlan.get(stack.time_axis, config.freq, config.harmonics, config.history,
                           config.bandwidth, crit, device, nan_mode=config.nan_mode)
     t_model = clock() - mark
 
-    n = config.history
-    if _is_cuda_tensor(stack.data):
+    if on_device:
         import torch
 
         mark = clock()
@@ -279,8 +282,12 @@ def _run(stack, config, threads, block_size, keep_mosum, return_beta, return_mea
                            detected=host(res.detected))
         t_ingest, t_d2h = 0.0, clock() - mark
     else:
-        res = plan.run_host(stack.data, keep_mosum=keep_mosum, beta=return_beta, mean=return_mean,
-                            ref_dtypes=True)
+        if source is None:
+            res = plan.run_host(stack.data, keep_mosum=keep_mosum, beta=return_beta, mean=return_mean,
+                                ref_dtypes=True)
+        else:
+            res = plan.run_file(source[0], source[1], stack.n_pixels, keep_mosum=keep_mosum, beta=return_beta,
+                                mean=return_mean, ref_dtypes=True)
         t_kernel = res.kernel_ms * 1e-3
         t_ingest = max(0.0, (res.total_ms - res.kernel_ms) * 1e-3)
         t_d2h = 0.0

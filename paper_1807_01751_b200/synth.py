@@ -126,3 +126,74 @@ def device_stack(n_pixels: int, t: np.ndarray, freq: float, n_hist: int, nan_fra
         blk[:, dead] = float("nan")
         out[:, p0:p0 + w] = blk
     return out
+
+
+# ---- the reference's benchmark recipe (CLI `generate` / `bench`) -------------------------
+# Restated from its documented contract (reference synth.py:29-105): a sine of amplitude
+# 0.05 with period `freq` plus N(0, noise_std^2) noise; the first floor(break_ratio * m)
+# pixels get +break_mag over the last floor(break_frac * N) dates.  Pixels are generated
+# in 4096-column blocks, block i drawing from Philox(key=seed, counter=i << 128), so files
+# written by `generate` are bit-identical to the reference's for the same flags.
+SYNTH_AMPLITUDE = 0.05
+SYNTH_BLOCK = 4096
+
+
+@dataclass(frozen=True)
+class SynthSpec:
+    n_pixels: int
+    n_obs: int
+    freq: float
+    noise_std: float = 0.01
+    break_mag: float = 0.1
+    break_frac: float = 0.4
+    break_ratio: float = 0.5
+    seed: int = 0
+
+    def __post_init__(self):
+        checks = [
+            (self.n_pixels >= 1, "n_pixels must be >= 1"),
+            (self.n_obs >= 2, "n_obs must be >= 2"),
+            (self.freq > 0, "freq must be positive"),
+            (self.noise_std >= 0, "noise_std must be >= 0"),
+            (0.0 <= self.break_frac <= 1.0, "break_frac must lie in [0, 1]"),
+            (0.0 <= self.break_ratio <= 1.0, "break_ratio must lie in [0, 1]"),
+            (0 <= self.seed < 2**64, "seed must be an unsigned 64-bit integer"),
+        ]
+        for ok, msg in checks:
+            if not ok:
+                raise ValueError(msg)
+
+
+def generate(spec: SynthSpec, threads: Optional[int] = None):
+    """(SeriesStack, truth) for a SynthSpec; deterministic per seed, any thread count."""
+    import math
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .engine import SeriesStack, resolve_threads
+    from .model import regular_axis
+
+    N, m = spec.n_obs, spec.n_pixels
+    t = np.arange(1.0, N + 1.0)
+    season = SYNTH_AMPLITUDE * np.sin(2.0 * np.pi * t / spec.freq)
+    n_break = int(math.floor(spec.break_ratio * m + 1e-9))
+    n_shift = int(math.floor(spec.break_frac * N + 1e-9))
+    out = np.empty((N, m), dtype=np.float32)
+
+    def block(i):
+        a, b = i * SYNTH_BLOCK, min(m, (i + 1) * SYNTH_BLOCK)
+        rng = np.random.Generator(np.random.Philox(key=spec.seed, counter=i << 128))
+        v = season[:, None] + spec.noise_std * rng.standard_normal((N, b - a))
+        k = min(b, n_break) - a
+        if k > 0 and n_shift > 0 and spec.break_mag != 0.0:
+            v[N - n_shift:, :k] += spec.break_mag
+        out[:, a:b] = v
+
+    n_blocks = (m + SYNTH_BLOCK - 1) // SYNTH_BLOCK
+    threads = resolve_threads(threads)
+    if threads > 1 and n_blocks > 1:
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            list(pool.map(block, range(n_blocks)))
+    else:
+        for i in range(n_blocks):
+            block(i)
+    return SeriesStack(out, regular_axis(N)), np.arange(m) < n_break

@@ -1,0 +1,86 @@
+"""BTS1 file -> GPU streaming path (dataio.monitor_file / bwm_monitor_file), on the GPU.
+
+monitor_file must give exactly the maps monitor_batch(read_stack(path)) gives — same kernel,
+same inputs — whatever the staging geometry: whole-stack mode, the chunked pipeline
+(BWM_HOST_CHUNK) and rectangles split inside a row (BWM_IO_SLOT_BYTES).  One golden case is
+also checked against the reference's own outputs through the file path.
+"""
+import numpy as np
+import pytest
+
+from tests.golden_cases import load
+from tests.test_gpu_parity import check_parity, config_for
+
+pytestmark = pytest.mark.gpu
+
+
+def _pkg():
+    import paper_1807_01751_b200 as pkg
+
+    return pkg
+
+
+def _same(a, b):
+    for f in ("detected", "first_break", "max_abs_mo", "valid"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    if a.mosum is not None:
+        assert np.array_equal(a.mosum, b.mosum)
+    if a.beta is not None:
+        assert np.array_equal(a.beta, b.beta)
+
+
+@pytest.mark.parametrize("name", ["c1", "irregular_h70"])
+def test_file_path_matches_reference_golden(tmp_path, name):
+    pkg = _pkg()
+    case = load(name)
+    path = tmp_path / "s.bts"
+    pkg.write_stack(pkg.SeriesStack(case.y, pkg.TimeAxis(case.t)), path)
+    bm = pkg.monitor_file(path, config_for(case))
+    check_parity(case, bm.first_break, bm.max_abs_mo, bm.valid)
+
+
+@pytest.mark.parametrize("env", [{}, {"BWM_HOST_CHUNK": "3000"}, {"BWM_IO_SLOT_BYTES": "4096"},
+                                 {"BWM_HOST_CHUNK": "2600", "BWM_IO_SLOT_BYTES": "1000"}])
+def test_file_equals_batch(tmp_path, monkeypatch, env):
+    pkg = _pkg()
+    case = load("c1")
+    path = tmp_path / "s.bts"
+    pkg.write_stack(pkg.SeriesStack(case.y[:, :9001], pkg.TimeAxis(case.t)), path)  # ragged tail tile
+    cfg = config_for(case)
+    ref = pkg.monitor_batch(pkg.read_stack(path), cfg, keep_mosum=True, return_beta=True)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = pkg.monitor_file(path, cfg, keep_mosum=True, return_beta=True)
+    _same(got, ref)
+
+
+def test_file_masked_mode(tmp_path):
+    pkg = _pkg()
+    case = load("c1")
+    path = tmp_path / "s.bts"
+    pkg.write_stack(pkg.SeriesStack(case.y, pkg.TimeAxis(case.t)), path)
+    from dataclasses import replace
+
+    cfg = replace(config_for(case), nan_mode="mask")
+    _same(pkg.monitor_file(path, cfg), pkg.monitor_batch(pkg.read_stack(path), cfg))
+
+
+def test_truncated_payload_raises(tmp_path):
+    pkg = _pkg()
+    case = load("c1")
+    path = tmp_path / "s.bts"
+    pkg.write_stack(pkg.SeriesStack(case.y[:, :100], pkg.TimeAxis(case.t)), path)
+    raw = path.read_bytes()
+    path.write_bytes(raw[:-4])
+    with pytest.raises(pkg.StackFormatError, match="truncated"):
+        pkg.monitor_file(path, config_for(case))
+
+
+def test_profile_file_phases(tmp_path):
+    pkg = _pkg()
+    case = load("c1")
+    path = tmp_path / "s.bts"
+    pkg.write_stack(pkg.SeriesStack(case.y, pkg.TimeAxis(case.t)), path)
+    bm, t = pkg.profile_file(path, config_for(case))
+    assert len(bm) == case.y.shape[1]
+    assert t.mosum > 0 and t.ingest > 0 and t.total >= t.mosum
