@@ -188,6 +188,8 @@ typedef struct bwm_plan_info_t {
     int32_t masked_global;    /* mask mode: x x^T table and residual rings in global memory          */
     int32_t ctas_per_sm_masked;
     int64_t smem_masked;      /* dynamic shared memory per CTA, masked kernel                        */
+    int32_t const_bound;      /* boundary constant over the monitoring period (LEAN TMA variant)     */
+    int32_t ctas_per_sm_tma_lean; /* persistent CTAs per SM, LEAN TMA variant                        */
 } bwm_plan_info_t;
 
 int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info);

@@ -93,8 +93,8 @@ int64_t smem_bytes_for(int N, int n, int h, int p, bool ring) {
     return bytes;
 }
 
-// TMA kernel ring mode for a bandwidth h (bwm_kernel_tma.cuh): a TMEM ring of L rows (+8
-// mirror rows, 2 columns each) when 8 <= h and it fits 256 columns; a shared-memory ring for
+// TMA kernel ring mode for a bandwidth h (bwm_kernel_tma.cuh): a TMEM ring of L rows (2
+// columns each) when 8 <= h and it fits 256 columns; a shared-memory ring for
 // h < 8; the lagging cursor above.
 struct TmaRing {
     int mode, rows, cols;
@@ -102,7 +102,7 @@ struct TmaRing {
 TmaRing tma_ring_for(int h) {
     constexpr int R = bwm::kStageRows;
     const int L = ((h + R - 1) / R) * R;
-    const int need = 2 * (L + R);
+    const int need = 2 * L;
     if (h >= R && need <= 256) {
         int cols = 32;
         while (cols < need) cols *= 2;
@@ -111,16 +111,14 @@ TmaRing tma_ring_for(int h) {
     return {h < R ? -1 : (int)bwm::kRingLag, 0, 0};   // -1: no TMA variant (LDG kernel)
 }
 
-// shared memory of the TMA kernel: stages + tables (mapping padded to 8-row stages, bound
-// indexed by row) + 2*kStages mbarriers + the TMEM address slot; 0 when no TMA variant applies
+// shared memory of the TMA kernel: per-warp stage rings + tables (Z^T, bound indexed by row) + the stage mbarriers + the TMEM address slot; 0 when no TMA variant applies
 int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
     (void)h;
     if (mode < 0) return 0;
     const int sp = (p + 3) & ~3;
-    const int n8 = ((n + bwm::kStageRows - 1) / bwm::kStageRows) * bwm::kStageRows;
-    int64_t fl = (int64_t)n8 * sp + (int64_t)N * sp + ((N + 3) & ~3);
+    int64_t fl = (int64_t)N * sp + ((N + 3) & ~3);     // Z^T (rows < n double as Q^T) + bound
     int64_t bytes = bwm::kWarps * bwm::kStages * bwm::tma_stage_bytes(mode) + fl * 4;
-    return bytes + bwm::kWarps * bwm::kStages * 8 + 16;
+    return bytes + bwm::kWarps * bwm::kStages * 8 + 16;  // + per-warp stage barriers, TMEM slot
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed).
@@ -247,6 +245,8 @@ struct bwm_plan {
     int blocks_per_sm[3] = {0, 0, 0};  // [Kind]
     int occ_raw[3] = {0, 0, 0};        // occupancy API result before the TMEM cap
     bool force_ldg = false;            // BWM_KERNEL=ldg (A/B against the TMA kernel)
+    bool const_bound = false;          // b_j == b_0 for every j (LEAN TMA variant applies)
+    int bpm_tma_lean = 0;              // resident CTAs per SM of the LEAN TMA variant
     // masked-NaN mode (bwm_kernel_masked.cuh)
     bool masked = false;
     bool mbig = false;                 // x x^T table + rings in global memory
@@ -493,7 +493,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         for (int i = 0; i < p; ++i) {      // z_t = R^-T x_t  <=>  z_t,i = sum_k Rinv[k][i] x_k,t
             double z = 0.0;
             for (int k = 0; k <= i; ++k) z += Rinv[(size_t)k * p + i] * tb->design[(size_t)k * N + t];
-            xt[(size_t)t * sp + i] = (float)z;
+            xt[(size_t)t * sp + i] = (float)(t < n ? Q[(size_t)t * p + i] : z);   // z_t == q_t for t < n
         }
     for (int j = 0; j < N - n; ++j) bd[j] = (float)tb->bound[j];
     for (size_t i = 0; i < ri.size(); ++i) ri[i] = (float)Rinv[i];
@@ -521,44 +521,46 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     if ((e = cudaMemcpy(plan->d_rinv, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
 
-    for (int v = 0; v < 3; ++v) {
-        const Kind kind = (Kind)v;
-        const int64_t sm = kind == kTma ? plan->smem_tma : plan->smem;
-        if (kind == kTma && sm == 0) continue;
-        KernelFn fn = pick(p, kind, kind == kTma ? plan->tring.mode : (plan->ring ? 0 : (int)bwm::kRingLag));
+    // LEAN TMA variant: the boundary is one value over the whole monitoring period
+    plan->const_bound = true;
+    for (int j = 1; j < N - n; ++j) plan->const_bound = plan->const_bound && bd[(size_t)j] == bd[0];
+
+    // per kernel: the dynamic shared-memory limit and the resident CTAs per SM
+    auto setup = [&](KernelFn fn, Kind kind, int64_t sm, int* nb_out) -> cudaError_t {
         // the limit is per-kernel global state shared by every plan: set it to the device
         // maximum once, never lower it (a later plan must not shrink an earlier plan's launch)
-        if ((e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      max_optin)) != cudaSuccess)
-            return fail(e, "cudaFuncSetAttribute");
+        cudaError_t err = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
+        if (err != cudaSuccess) return err;
         int nb = 0;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, threads_of(kind),
-                                                               (size_t)sm)) != cudaSuccess)
-            return fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+        if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, threads_of(kind), (size_t)sm)) !=
+            cudaSuccess)
+            return err;
         if (kind == kTma && plan->tring.mode == bwm::kRingTmem) {
             // The occupancy API assumes a kernel that allocates Tensor Memory owns the SM's
             // TMEM (reports 1).  Allocation is dynamic (tcgen05.alloc + relinquish_alloc_permit),
             // so residency is bounded by registers, shared memory, threads and our own column
             // budget: 512 columns per SM / tmem_cols per CTA.
-            cudaFuncAttributes fa{};
-            if ((e = cudaFuncGetAttributes(&fa, (const void*)fn)) != cudaSuccess)
-                return fail(e, "cudaFuncGetAttributes");
-            int regs_per_sm = 0, smem_per_sm = 0, reserved = 0, max_threads = 0;
-            cudaDeviceGetAttribute(&regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, device);
-            cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
-            cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
-            cudaDeviceGetAttribute(&max_threads, cudaDevAttrMaxThreadsPerMultiProcessor, device);
-            const int thr = threads_of(kind);
-            const int warps = (thr + 31) / 32;
-            const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;     // per-warp allocation unit
-            const int by_regs = regs_per_sm / (regs_warp * warps);
-            const int by_smem = (int)(smem_per_sm / (sm + (int64_t)fa.sharedSizeBytes + reserved));
-            const int by_thr = max_threads / thr;
-            const int by_tmem = 512 / plan->tring.cols;
-            nb = std::min(std::min(by_regs, by_smem), std::min(by_thr, by_tmem));
+            nb = resident_ctas((const void*)fn, threads_of(kind), sm, plan->tring.cols, device, &err);
+            if (err != cudaSuccess) return err;
         }
+        *nb_out = nb;
+        return cudaSuccess;
+    };
+    for (int v = 0; v < 3; ++v) {
+        const Kind kind = (Kind)v;
+        const int64_t sm = kind == kTma ? plan->smem_tma : plan->smem;
+        if (kind == kTma && sm == 0) continue;
+        int nb = 0;
+        if ((e = setup(pick(p, kind, kind == kTma ? plan->tring.mode : (plan->ring ? 0 : (int)bwm::kRingLag)), kind,
+                       sm, &nb)) != cudaSuccess)
+            return fail(e, "kernel setup");
         plan->occ_raw[v] = nb;
         plan->blocks_per_sm[v] = std::max(nb, 1);
+        if (kind == kTma) {
+            if ((e = setup(pick(p, kind, plan->tring.mode | bwm::kTmaLean), kind, sm, &nb)) != cudaSuccess)
+                return fail(e, "kernel setup");
+            plan->bpm_tma_lean = std::max(nb, 1);
+        }
     }
     *out_plan = plan;
     return BWM_OK;
@@ -687,9 +689,12 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         kp.beta = out->beta ? out->beta + p0 : nullptr;
         kp.mo_mean = out->mo_mean ? out->mo_mean + p0 : nullptr;
         kp.mosum = out->mosum ? out->mosum + p0 : nullptr;
-        KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode : (plan->ring ? 0 : (int)bwm::kRingLag));
+        const bool lean = kind == kTma && plan->const_bound && !out->mosum && !out->mo_mean;
+        KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode | (lean ? bwm::kTmaLean : 0)
+                                                          : (plan->ring ? 0 : (int)bwm::kRingLag));
         const int64_t tiles = (cnt + bwm::kTile - 1) / bwm::kTile;
-        const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * plan->blocks_per_sm[kind]);
+        const int bpm = lean ? plan->bpm_tma_lean : plan->blocks_per_sm[kind];
+        const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * bpm);
         const size_t sm = (size_t)(kind == kTma ? plan->smem_tma : plan->smem);
         if (kind == kTma) {
             int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y);
@@ -1010,6 +1015,8 @@ int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {
     info->masked_global = plan->mbig ? 1 : 0;
     info->ctas_per_sm_masked = plan->bpm_masked;
     info->smem_masked = plan->smem_masked;
+    info->const_bound = plan->const_bound ? 1 : 0;
+    info->ctas_per_sm_tma_lean = plan->bpm_tma_lean;
     return BWM_OK;
 }
 

@@ -7,10 +7,12 @@
 namespace bwm {
 enum Kind { kLdgFast = 0, kLdgSafe = 1, kTma = 2 };
 using KernelFn = void (*)(const KParams);
+constexpr int kTmaLean = 0x10;   // pick(): OR into the TMA ring mode for the LEAN variant
 }  // namespace bwm
 
 // Defines bwm::KernelFn bwm_pick_p<NP>(int kind, int mode) in the including TU.
-// mode: bwm::RingMode of the TMA kernel (kRingTmem / kRingLag; < 0 = none); the LDG kernels
+// mode: bwm::RingMode of the TMA kernel (kRingTmem / kRingLag; < 0 = none), | kTmaLean for the
+// LEAN variant (no MOSUM matrix/mean, constant boundary); the LDG kernels
 // have a shared-memory ring (any mode but kRingLag) or the lagging cursor.
 #define BWM_DEFINE_PICK(NP)                                                                      \
     bwm::KernelFn bwm_pick_p##NP(int kind, int mode) {                                           \
@@ -21,8 +23,11 @@ using KernelFn = void (*)(const KParams);
             case bwm::kLdgSafe:                                                                  \
                 return ring ? bwm::monitor_kernel_ldg<NP, true, true> : bwm::monitor_kernel_ldg<NP, true, false>;   \
             default:                                                                             \
-                return mode == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem>      \
-                                              : bwm::monitor_kernel_tma<NP, bwm::kRingLag>;      \
+                if (mode & bwm::kTmaLean)                                                        \
+                    return (mode & 0xF) == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem, true> \
+                                                          : bwm::monitor_kernel_tma<NP, bwm::kRingLag, true>; \
+                return (mode & 0xF) == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem, false> \
+                                                      : bwm::monitor_kernel_tma<NP, bwm::kRingLag, false>; \
         }                                                                                        \
     }
 
