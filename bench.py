@@ -49,6 +49,8 @@ def parse():
                     help="fill: the reference's gap fill (headline); mask: per-pixel masked fits (extension)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-file", action="store_true",
+                    help="also time monitor_file on a BTS1 copy of the stack (page cache: /dev/shm or /tmp)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 20, help="pixels in the CPU baseline sample")
     return ap.parse_args()
@@ -218,6 +220,46 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def e2e_file(ynp, t, cfg, steps, world):
+    """monitor_file on a BTS1 file of the same stack (dataio.monitor_file -> bwm_monitor_file):
+    file read (page cache) + H2D + kernel + D2H; the file lives in /dev/shm (RAM) when it fits."""
+    import shutil
+    import tempfile
+
+    from paper_1807_01751_b200 import SeriesStack, TimeAxis, monitor_file, write_stack
+
+    need = ynp.nbytes + (1 << 30)
+    for d in ("/dev/shm", tempfile.gettempdir()):
+        try:
+            if shutil.disk_usage(d).free > need:
+                break
+        except OSError:
+            continue
+    else:
+        return {"skipped": f"no directory with {need / 1e9:.1f} GB free"}
+    path = os.path.join(d, f"bench_{os.getpid()}.bts")
+    try:
+        t0 = time.perf_counter()
+        write_stack(SeriesStack(ynp, TimeAxis(t)), path)
+        t_write = time.perf_counter() - t0
+        monitor_file(path, cfg)                               # warm: staging slots, plan
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            bm = monitor_file(path, cfg)
+        dt = max_over_ranks(time.perf_counter() - t0, world)
+        assert bm.break_count > 0
+        return {"value": world * ynp.shape[1] * steps / dt / 1e6, "unit": UNIT, "ms_per_step": 1e3 * dt / steps,
+                "file_gb": ynp.nbytes / 1e9, "dir": d, "write_s": t_write,
+                "path": "monitor_file(BTS1 path): pread row blocks into pinned slots (reader threads) "
+                        "overlapped with H2D, kernel, finalize, D2H"}
+    finally:
+        try:
+            os.remove(path)
+        except OSError:
+            pass
+
+
 def run_ours(args):
     import torch
 
@@ -297,6 +339,8 @@ def run_ours(args):
                        "stack, one kernel launch, device-side finalize to the reference dtypes, D2H of "
                        "valid/detected/first_break(int64)/max_abs_mo(float64)"}
         assert bm.break_count > 0
+        if args.e2e_file:
+            e2e["file"] = e2e_file(ynp, t, cfg, args.e2e_steps, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
