@@ -144,7 +144,7 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
  * the caller parsed — the plan's time axis comes from it).  io_threads threads pread row
  * blocks of the payload into pinned staging slots while earlier blocks are copied to HBM, so
  * the file read, the PCIe transfer and (for stacks larger than device memory) the kernel
- * overlap.  io_threads < 1: min(8, hardware threads).  Outputs as for bwm_monitor_host.
+ * overlap.  io_threads < 1: min(32, hardware threads).  Outputs as for bwm_monitor_host.
  * Returns BWM_E_IO / BWM_E_FORMAT for unreadable or truncated files.
  */
 int bwm_monitor_file(bwm_plan* plan, const char* path, int64_t payload_offset, int64_t n_pixels,

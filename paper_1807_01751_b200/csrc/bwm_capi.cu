@@ -838,7 +838,7 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
             rect_begin.push_back((int64_t)rects.size());
         }
         const int threads = std::max(1, io_threads);
-        K = std::max(4, std::min(threads + 4, 24));
+        K = std::max(4, std::min(threads + 4, 40));
         std::string err;
         if (int e = reader.ensure(K, slot_bytes, &err)) return set_err(e, "%s", err.c_str());
         slot_ev.resize((size_t)K, nullptr);
@@ -995,7 +995,7 @@ int bwm_monitor_file(bwm_plan* plan, const char* path, int64_t payload_offset, i
     bwm::PayloadFile f;
     std::string err;
     if (int rc = f.open(path, payload_offset, plan->dims.n_obs, n_pixels, &err)) return set_err(rc, "%s", err.c_str());
-    if (io_threads < 1) io_threads = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency()));
+    if (io_threads < 1) io_threads = (int)std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
     return monitor_pipeline(plan, nullptr, n_pixels, &f, io_threads, n_pixels, 0, out_host);
 }
 
