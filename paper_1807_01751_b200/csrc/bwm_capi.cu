@@ -116,7 +116,8 @@ int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
     (void)h;
     if (mode < 0) return 0;
     const int sp = (p + 3) & ~3;
-    int64_t fl = (int64_t)N * sp + ((N + 3) & ~3);     // Z^T (rows < n double as Q^T) + bound
+    // Z^T (rows < n double as Q^T; global memory in the lagging-cursor mode) + bound
+    int64_t fl = (mode == bwm::kRingLag ? 0 : (int64_t)N * sp) + ((N + 3) & ~3);
     int64_t bytes = bwm::kWarps * bwm::kStages * bwm::tma_stage_bytes(mode) + fl * 4;
     return bytes + bwm::kWarps * bwm::kStages * 8 + 16;  // + per-warp stage barriers, TMEM slot
 }

@@ -188,13 +188,18 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : 2)
     unsigned char* s_stage = smem_raw;                                   // [kWarps][S][SB]
     // [N][SP] Z^T: fitted-value rows; for t < n they are the rows of Q (host: bwm_plan_create),
     // so pass 1 reads its basis from the same table (full stages only touch rows < n)
-    float* s_xt = reinterpret_cast<float*>(smem_raw + kWarps * S * SB);
+    // kRingLag (large h, C4): the tables stay in global memory and are read through L1 (uniform
+    // addresses, broadcast) so that two CTAs fit per SM next to the double-box stage rings.
+    constexpr bool kTblSmem = MODE != kRingLag;
+    float* s_tbl = reinterpret_cast<float*>(smem_raw + kWarps * S * SB);
+    const float* s_xt = kTblSmem ? s_tbl : prm.xt;
     const float* s_mt = s_xt;
-    float* s_bd = s_xt + N * SP;                                         // [NA] bound by row t (t >= n)
+    float* s_bd = s_tbl + (kTblSmem ? N * SP : 0);                       // [NA] bound by row t (t >= n)
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);           // [kWarps][S]
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + kWarps * S);
 
-    for (int i = threadIdx.x; i < N * SP; i += kTmaThreads) s_xt[i] = prm.xt[i];
+    if (kTblSmem)
+        for (int i = threadIdx.x; i < N * SP; i += kTmaThreads) s_tbl[i] = prm.xt[i];
     for (int i = threadIdx.x; i < N - n; i += kTmaThreads) s_bd[n + i] = prm.bound[i];
     if (threadIdx.x == 0) {
         for (int s = 0; s < kWarps * S; ++s) mbar_init(s_bar + s, 1);
