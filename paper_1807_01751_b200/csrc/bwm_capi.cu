@@ -118,8 +118,9 @@ int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
     const int sp = (p + 3) & ~3;
     // Z^T (rows < n double as Q^T; global memory in the lagging-cursor mode) + bound
     int64_t fl = (mode == bwm::kRingLag ? 0 : (int64_t)N * sp) + ((N + 3) & ~3);
-    int64_t bytes = bwm::kWarps * bwm::kStages * bwm::tma_stage_bytes(mode) + fl * 4;
-    return bytes + bwm::kWarps * bwm::kStages * 8 + 16;  // + per-warp stage barriers, TMEM slot
+    const int S = bwm::stages_for(mode);
+    int64_t bytes = bwm::kWarps * S * bwm::tma_stage_bytes(mode) + fl * 4;
+    return bytes + bwm::kWarps * S * 8 + 16;              // + per-warp stage barriers, TMEM slot
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed).

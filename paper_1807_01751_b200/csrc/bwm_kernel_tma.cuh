@@ -47,7 +47,12 @@ namespace bwm {
 #define BWM_STAGES 5
 #endif
 constexpr int kStageRows = BWM_STAGE_ROWS;      // dates per stage (multiple of 8)
-constexpr int kStages = BWM_STAGES;             // stage ring depth per warp
+#ifndef BWM_STAGES_LAG
+#define BWM_STAGES_LAG 3
+#endif
+constexpr int kStages = BWM_STAGES;             // stage ring depth per warp (TMEM-ring mode)
+// the lagging-cursor mode moves two boxes per stage (dates t and t-h): 3 stages = 6 boxes
+__host__ __device__ constexpr int stages_for(int mode) { return mode == 2 /* kRingLag */ ? BWM_STAGES_LAG : kStages; }
 static_assert(kStageRows == 8 || kStageRows == 16, "stage height: 8 or 16 dates (compensation blocks are 16)");
 constexpr int kWarpPx = 64;                     // pixels per warp slice (32 lanes x 2)
 constexpr int kBoxBytes = kStageRows * kWarpPx * 4;
@@ -169,17 +174,20 @@ __host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
 #ifndef BWM_TMA_MINB
 #define BWM_TMA_MINB 4
 #endif
+#ifndef BWM_TMA_MINB_BIG
+#define BWM_TMA_MINB_BIG 3
+#endif
 // LEAN: no MOSUM matrix / MOSUM mean outputs and a constant boundary over the monitoring
 // period (b_j = lambda for every j: log_plus((n+1+j)/n) = 1 while (n+1+j)/n <= e, which holds
 // for all BASELINE geometries, N/n = 2) — the per-date boundary product, mean accumulation
 // and output branch drop out of the MOSUM loop.  Results are bit-identical to !LEAN.
 template <int NP, int MODE, bool LEAN>
-__global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : 2)
+__global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA_MINB_BIG)
     monitor_kernel_tma(const __grid_constant__ KParams prm) {
     static_assert(MODE == kRingTmem || MODE == kRingLag, "TMA kernel: TMEM ring or lagging cursor");
     constexpr int SP = Coefs<NP>::SP;
     constexpr int R = kStageRows;
-    constexpr int S = kStages;
+    constexpr int S = stages_for(MODE);
     constexpr int64_t SB = tma_stage_bytes(MODE);
     constexpr int ROWF2 = kWarpPx / 2;           // float2 per staged row of a warp slice
     extern __shared__ __align__(128) unsigned char smem_raw[];
