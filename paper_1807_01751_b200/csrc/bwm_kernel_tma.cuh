@@ -235,7 +235,8 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
     // re-arming a slot is a lookup.  The slot being re-armed was read by this warp through
     // the generic proxy; __syncwarp() in release() orders those reads before lane 0 issues
     // the copy (the same release->acquire ordering an mbarrier handshake gives a producer).
-    const int st1 = (n + R - 1) / R, st2 = (n - w0 + R - 1) / R;
+    // TMEM mode has no pass-2 stages: pass 1 parks the filled window-0 dates in the ring
+    const int st1 = (n + R - 1) / R, st2 = MODE == kRingTmem ? 0 : (n - w0 + R - 1) / R;
     const int tile_stages = st1 + st2 + (N - t3 + R - 1) / R;
     int64_t itile = blockIdx.x;
     int istage = 0, islot = 0;
@@ -344,18 +345,25 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
             }
             // rows >= n of the last stage: zero mapping rows (exact no-ops) and no q update; the
             // fill state they leave behind is reset before pass 2
+            // TMEM mode: the filled values of the dates [w0, n) also go to their ring rows
+            // (t mod L); they become the window-0 residuals once beta is known (no re-read)
+            const bool park = MODE == kRingTmem && t0 >= w0;
             if (t0 + R <= n) {
                 const float* mrow = s_mt + t0 * SP;
+                float2 yy[R];
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const float2 vc = fill(st[k * ROWF2], negc, last);
+                    yy[k] = vc;
                     axpy_row<NP, SP>(part, vc, mrow + k * SP);
                     qpart = fma2(vc, vc, qpart);
                 }
+                if (park) ring_store(t0 % L, yy);
             } else {                                            // last stage: dates [t0, n) only
 #pragma unroll 1
                 for (int k = 0; k < n - t0; ++k) {
                     const float2 vc = fill(st[k * ROWF2], negc, last);
+                    if (park) ring_put_row((t0 + k) % L, vc);
                     axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
                     qpart = fma2(vc, vc, qpart);
                 }
@@ -385,12 +393,40 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
         const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);
 
-        // ---- pass 2: residuals of the last history rows -> ring and window 0 --------------
+        // ---- window 0 ------------------------------------------------------------------
         float2 acc = f2(0.f, 0.f);
-        last = lastw;
         float2 lag_last = w0 == wstart ? lastw : f2(0.f, 0.f);   // kRingLag: fill state at wstart-1
-        int wb = MODE == kRingTmem ? w0 % L : 0;
-        for (int t0 = w0; t0 < n; t0 += R) {
+        int wb = 0;
+        if (MODE == kRingTmem) {
+            // The ring rows of the dates [wstart, n) (row = date mod L, written in pass 1; h - 1
+            // < L rows, so none was overwritten) hold the filled values: convert them in place to
+            // the residuals r = y - z^T beta_Q, summing window 0 in date order — the arithmetic
+            // of a re-read pass, without re-reading.  R rows per batch, one .x2 access per row.
+            tmem_wait_st();
+            int q = wstart % L;
+#pragma unroll 1
+            for (int t0 = wstart; t0 < n; t0 += R) {
+                float2 v[R];
+                int qk[R];
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    qk[k] = q + k >= L ? q + k - L : q + k;
+                    if (t0 + k < n) ring_ld2(qk[k], v[k]);
+                }
+                tmem_wait_ld();
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    if (t0 + k < n) {
+                        const float2 r = dot_row<NP, SP>(v[k], s_xt + (t0 + k) * SP, nb);
+                        acc = add2(acc, r);
+                        ring_put_row(qk[k], r);
+                    }
+                }
+                q = q + R >= L ? q + R - L : q + R;
+            }
+        }
+        if (MODE == kRingLag) last = lastw;                     // pass 2 re-reads [w0, n)
+        for (int t0 = w0; MODE == kRingLag && t0 < n; t0 += R) {
             const float2* st = acquire();
             if (t0 + R <= n) {
                 float2 rr[R];
