@@ -314,6 +314,27 @@ def run_ours(args):
     if z != _lib.INT64_MAX:
         raise RuntimeError(f"synthetic stack produced a zero-sigma pixel {z}")
 
+    # ---- whole-box result maps (N > 1): one gather of the 9 B/px device maps, timed apart ----
+    gather = None
+    if world > 1:
+        import torch.distributed as dist
+
+        from paper_1807_01751_b200.sharding import gather_device_maps
+
+        on_dev = dist.get_backend() == "nccl"
+        mv = [res.valid, res.first_idx, res.max_abs] if on_dev else [res.valid.cpu(), res.first_idx.cpu(),
+                                                                     res.max_abs.cpu()]
+        barrier(world)
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        maps = gather_device_maps(*mv, rank, world)
+        torch.cuda.synchronize()
+        g_ms = max_over_ranks((time.perf_counter() - g0) * 1e3, world)
+        gather = {"ms": g_ms, "bytes": world * P * 9, "collective": "all_gather of packed u8/i32/f32 maps "
+                  f"({dist.get_backend()})", "note": "whole-box maps on rank 0; not part of the step"}
+        if rank == 0:
+            assert int(maps[0].numel()) == world * P
+
     # ---- end to end through the public API: pinned host stack -> BreakMap ------------------
     e2e = None
     if not args.no_e2e:
@@ -381,6 +402,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),
+            "gather": gather,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)

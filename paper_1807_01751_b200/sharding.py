@@ -70,3 +70,34 @@ def gather_maps(local: dict, rank: int, world: int, group=None) -> Optional[dict
             full = np.concatenate([p[:s].cpu().numpy() for p, s in zip(parts, sizes)])
             out[key] = full.astype(arr.dtype)
     return out if rank == 0 else None
+
+
+def gather_device_maps(valid, first_idx, max_abs, rank: int, world: int, group=None):
+    """Whole-box result maps on rank 0 from the per-rank DEVICE maps (the kernel's raw u8 /
+    i32 / f32 outputs, 9 B per pixel), packed into one byte tensor per rank and gathered with
+    one collective over NVLink (NCCL; gloo with CPU tensors in the tests).  Returns
+    (valid, first_idx, max_abs) tensors on rank 0 in global pixel order, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return valid, first_idx, max_abs
+    n = int(valid.numel())
+    packed = torch.cat([first_idx.contiguous().view(torch.uint8), max_abs.contiguous().view(torch.uint8),
+                        valid.contiguous().view(torch.uint8)])          # 4-byte fields first: aligned views
+    sizes = [torch.zeros(1, dtype=torch.int64, device=valid.device) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=valid.device), group=group)
+    sizes = [int(s.item()) for s in sizes]
+    width = 9 * max(sizes)
+    buf = torch.zeros(width, dtype=torch.uint8, device=valid.device)
+    buf[: packed.numel()] = packed
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    if rank != 0:
+        return None
+    v, f, m = [], [], []
+    for p, s in zip(parts, sizes):
+        f.append(p[:4 * s].view(torch.int32))
+        m.append(p[4 * s:8 * s].view(torch.float32))
+        v.append(p[8 * s:9 * s])
+    return torch.cat(v), torch.cat(f), torch.cat(m)

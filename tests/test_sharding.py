@@ -72,3 +72,45 @@ def test_gloo_two_rank_gather_matches_unsharded():
     # the float64 oracle's BLAS rounding depends on block width; the GPU kernel itself is
     # bit-identical under any sharding (test_gpu_parity.py::test_shard_invariance)
     np.testing.assert_allclose(got["max_abs_mo"], ref.max_abs_mo, rtol=1e-12, atol=0)
+
+
+def _worker_dev(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1807_01751_b200.sharding import gather_device_maps
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 5 + 3 * rank                      # ragged shards
+        base = 100 * rank
+        valid = torch.tensor([(base + i) % 2 for i in range(n)], dtype=torch.uint8)
+        first = torch.arange(base, base + n, dtype=torch.int32)
+        mx = torch.arange(base, base + n, dtype=torch.float32) * 0.5
+        out = gather_device_maps(valid, first, mx, rank, world)
+        if rank == 0:
+            q.put([t.numpy().copy() for t in out])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_device_map_gather():
+    """The packed-byte gather bench.py uses for whole-box maps (NCCL on the GPU box)."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_dev, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    v, f, m = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_f = np.concatenate([np.arange(0, 5), np.arange(100, 108)]).astype(np.int32)
+    assert np.array_equal(f, want_f)
+    assert np.array_equal(m, want_f.astype(np.float32) * 0.5)
+    assert np.array_equal(v, (want_f % 2).astype(np.uint8))
