@@ -1,0 +1,85 @@
+"""Parity at BASELINE.json's full single-GPU sizes (C2: 4096^2 px x 228 dates, C4: 2048^2 px
+x 1000 dates, C5: 7000^2 px x 400 dates), where the float64 oracle cannot run on everything:
+
+  * a seeded random sample of pixels, copied back to the host, against the oracle
+    (same tolerances as test_gpu_parity.py: valid identical, first_break identical off the
+    boundary, max_abs_mo rtol 1e-4);
+  * size-independent properties on the WHOLE stack: placement invariance (the view starting
+    s pixels in gives the shifted maps) and shard invariance (two parts == whole), bit for bit;
+  * sanity of the break statistics of the synthetic NDVI stacks (half the pixels carry a
+    level drop inside the monitoring period; dead pixels are invalid).
+"""
+import numpy as np
+import pytest
+
+from oracle import bfast_oracle as bo
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+
+
+def _setup(name):
+    import torch
+
+    from paper_1807_01751_b200.device import DevicePlan
+    from paper_1807_01751_b200.model import TimeAxis
+    from paper_1807_01751_b200.synth import WORKLOADS, device_stack, time_axis
+
+    w = WORKLOADS[name]
+    t = time_axis(w)
+    plan = DevicePlan(TimeAxis(t), w.freq, w.harmonics, w.n_hist, w.bandwidth, w.crit, "cuda")
+    y = device_stack(w.n_pixels, t, w.freq, w.n_hist, w.nan_frac, seed=20261017, device="cuda")
+    torch.cuda.synchronize()
+    return w, t, plan, y
+
+
+def _maps(res):
+    return [a.cpu().numpy() for a in (res.valid, res.first_idx, res.max_abs)]
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_fullsize_sample_against_oracle(name):
+    import torch
+
+    w, t, plan, y = _setup(name)
+    valid, first, mx = _maps(plan.run_device(y))
+    rng = np.random.default_rng(7)
+    idx = np.sort(rng.choice(w.n_pixels, size=6000, replace=False))
+    ys = y[:, torch.as_tensor(idx, device="cuda")].cpu().numpy()
+    del y
+    torch.cuda.empty_cache()
+    ref = bo.monitor(ys, t, w.n_hist, w.bandwidth, w.harmonics, w.freq, w.crit, keep_mosum=True)
+    assert np.array_equal(valid[idx].astype(bool), ref.valid)
+    bound = bo.boundary(w.n_hist, w.n_obs, w.crit)
+    pairs = bo.near_pairs(ref.mosum, bound)
+    border = bo.borderline_from_pairs(pairs, w.n_obs - w.n_hist, idx.size, ref.first_idx, first[idx])
+    bad = np.flatnonzero((first[idx] != ref.first_idx) & ~border & ref.valid)
+    assert bad.size == 0, f"{bad.size} non-borderline mismatches, e.g. pixels {idx[bad[:5]]}"
+    filled, _ = bo.fill_block(ys)
+    degen = (filled[:w.n_hist] == filled[0]).all(axis=0)       # constant history: sigma = 0 here
+    v = ref.valid & ~degen
+    np.testing.assert_allclose(mx[idx][v], ref.max_abs_mo[v], rtol=RTOL, atol=0)
+    # synthetic statistics: roughly half the valid pixels break, dead pixels are invalid
+    frac = (first[valid.astype(bool)] > 0).mean()
+    assert 0.3 < frac < 0.9, frac          # C4/C5 use an uncalibrated lambda = 3 (more alarms)
+    assert valid.mean() > 0.99
+
+
+@pytest.mark.parametrize("name", ["C2", "C5"])
+def test_fullsize_shift_and_shards(name):
+    """Pixel-placement invariance on the whole stack, without copies: monitoring the view that
+    starts s pixels in (a different tile / warp slice / lane for every pixel; s = 4 mod 256
+    keeps the TMA path) gives the maps of the whole stack shifted by s, and so do two shards."""
+    w, t, plan, y = _setup(name)
+    P = w.n_pixels
+    base = _maps(plan.run_device(y))
+    s = 256 * 1001 + 4
+    got = _maps(plan.run_device(y[:, s:], pixel_offset=s))
+    for a, b in zip(base, got):
+        assert np.array_equal(a[s:], b)
+    cut = (P // 3) // 2 * 2 + 2                      # 8-byte aligned: LDG path for the upper shard
+    lo = _maps(plan.run_device(y[:, :cut]))
+    hi = _maps(plan.run_device(y[:, cut:], pixel_offset=cut))
+    for a, b, c in zip(base, lo, hi):
+        assert np.array_equal(a, np.concatenate([b, c]))

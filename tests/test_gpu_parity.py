@@ -134,6 +134,10 @@ def test_kernel_variants_bit_identical(name, monkeypatch):
     for a, b, c in zip(tma, ldg, safe):
         assert np.array_equal(a, b)
         assert np.array_equal(a, c)
+    # the LEAN TMA variant (no mean/MOSUM outputs requested; constant boundary hoisted)
+    lean = _maps(_plan(case).run_device(y))
+    for a, b in zip(lean[:3], ldg[:3]):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("shards", [2, 3, 8])
