@@ -120,7 +120,8 @@ int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
     int64_t fl = (mode == bwm::kRingLag ? 0 : (int64_t)N * sp) + ((N + 3) & ~3);
     const int S = bwm::stages_for(mode);
     int64_t bytes = bwm::kWarps * S * bwm::tma_stage_bytes(mode) + fl * 4;
-    return bytes + bwm::kWarps * S * 8 + 16;              // + per-warp stage barriers, TMEM slot
+    const int sched = 2 * ((N + bwm::kStageRows - 1) / bwm::kStageRows) + 4;   // stage schedule table
+    return bytes + bwm::kWarps * S * 8 + 16 + 4 * sched;  // + per-warp stage barriers, TMEM slot
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed).

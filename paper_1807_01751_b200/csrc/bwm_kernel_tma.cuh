@@ -205,10 +205,21 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
     float* s_bd = s_tbl + (kTblSmem ? N * SP : 0);                       // [NA] bound by row t (t >= n)
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);           // [kWarps][S]
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + kWarps * S);
+    int* s_rows = reinterpret_cast<int*>(s_tmem + 4);                   // [tile_stages] stage -> first date
 
     if (kTblSmem)
         for (int i = threadIdx.x; i < N * SP; i += kTmaThreads) s_tbl[i] = prm.xt[i];
     for (int i = threadIdx.x; i < N - n; i += kTmaThreads) s_bd[n + i] = prm.bound[i];
+    {
+        // the per-tile stage schedule (identical for every tile): pass 1 [0, n), pass 2 [w0, n)
+        // (lagging-cursor mode only), pass 3 [8 floor(n/8), N), R dates per stage
+        const int w0_ = ((n - h + 1) / kStageRows) * kStageRows, t3_ = (n / kStageRows) * kStageRows;
+        const int a = (n + kStageRows - 1) / kStageRows;
+        const int b = a + (MODE == kRingTmem ? 0 : (n - w0_ + kStageRows - 1) / kStageRows);
+        const int c = b + (N - t3_ + kStageRows - 1) / kStageRows;
+        for (int i = threadIdx.x; i < c; i += kTmaThreads)
+            s_rows[i] = i < a ? i * kStageRows : i < b ? w0_ + (i - a) * kStageRows : t3_ + (i - b) * kStageRows;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kWarps * S; ++s) mbar_init(s_bar + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -238,23 +249,27 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
     // TMEM mode has no pass-2 stages: pass 1 parks the filled window-0 dates in the ring
     const int st1 = (n + R - 1) / R, st2 = MODE == kRingTmem ? 0 : (n - w0 + R - 1) / R;
     const int tile_stages = st1 + st2 + (N - t3 + R - 1) / R;
+    // The slot re-armed at a release is the one just consumed, so the issue cursor needs only
+    // (tile, stage); the first date of a stage comes from the schedule table.
     int64_t itile = blockIdx.x;
-    int istage = 0, islot = 0;
-    auto issue = [&]() {
+    int istage = 0;
+    int xw = (int)(itile * kTile) + wu * kWarpPx;           // x of the cursor's tile slice
+    auto issue_into = [&](int slot) {
         if (itile >= n_tiles) return;
-        const int r0 = istage < st1 ? istage * R : istage < st1 + st2 ? w0 + (istage - st1) * R
-                                                                        : t3 + (istage - st1 - st2) * R;
-        const int x = (int)(itile * kTile) + wu * kWarpPx;
-        const uint32_t dst = stage_u32 + (uint32_t)(islot * SB), bar = bar_u32 + (uint32_t)(islot * 8);
+        const int r0 = s_rows[istage];
+        const uint32_t dst = stage_u32 + (uint32_t)(slot * SB), bar = bar_u32 + (uint32_t)(slot * 8);
         if (MODE == kRingLag && istage >= st1 + st2)
-            tma_box2_elect(dst, &prm.tmap, x, r0, r0 - h, bar, 2 * kBoxBytes);   // + dates t-h (<0: zero fill)
+            tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBoxBytes);   // + dates t-h (<0: zero fill)
         else
-            tma_box_elect(dst, &prm.tmap, x, r0, bar, kBoxBytes);
-        if (++istage == tile_stages) { istage = 0; itile += gridDim.x; }
-        if (++islot == S) islot = 0;
+            tma_box_elect(dst, &prm.tmap, xw, r0, bar, kBoxBytes);
+        if (++istage == tile_stages) {
+            istage = 0;
+            itile += gridDim.x;
+            xw += (int)gridDim.x * kTile;
+        }
     };
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap)) : "memory");
-    for (int s = 0; s < S; ++s) issue();
+    for (int s = 0; s < S; ++s) issue_into(s);
 
     const int L = prm.ring_rows;
     const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(wu * 32) << 16) : 0u;
@@ -305,7 +320,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
     };
     auto release = [&]() {
         __syncwarp();
-        issue();                                     // re-arm this slot kStages ahead
+        issue_into(cur);                             // re-arm this slot kStages ahead
         if (++cur == S) { cur = 0; ph ^= 1; }
     };
 
