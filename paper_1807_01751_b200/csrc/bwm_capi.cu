@@ -87,7 +87,8 @@ constexpr int kRingMaxH = 64;   // ring in smem up to h = 64 (64 KB); above: lag
 // shared memory of the LDG kernel: tables + MOSUM ring
 int64_t smem_bytes_for(int N, int n, int h, int p, bool ring) {
     const int sp = (p + 3) & ~3;
-    int64_t fl = (int64_t)n * sp + (int64_t)N * sp + (((N - n) + 3) & ~3);
+    // ring variants stage the coefficient tables; lagging-cursor variants read them from L1
+    int64_t fl = (ring ? (int64_t)n * sp + (int64_t)N * sp : 0) + (((N - n) + 3) & ~3);
     int64_t bytes = fl * 4;
     if (ring) bytes += (int64_t)h * bwm::kThreads * 8;
     return bytes;
@@ -409,9 +410,15 @@ int64_t bwm_smem_bytes(const bwm_dims* d) {
         return small <= kMaskedSmemMax ? small
                                        : bwm::masked_smem_bytes(d->n_obs, d->n_hist, d->bandwidth, d->n_params, true);
     }
-    const bool ring = d->bandwidth <= kRingMaxH;
-    const int64_t tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, tma_ring_for(d->bandwidth).mode);
-    return tma > 0 ? tma : smem_bytes_for(d->n_obs, d->n_hist, d->bandwidth, d->n_params, ring);
+    constexpr int64_t kOptin = 232448;                 // sm_100 opt-in limit per CTA (no device here)
+    bool ring = d->bandwidth <= kRingMaxH;
+    int64_t ldg = smem_bytes_for(d->n_obs, d->n_hist, d->bandwidth, d->n_params, ring);
+    if (ldg > kOptin && ring) ldg = smem_bytes_for(d->n_obs, d->n_hist, d->bandwidth, d->n_params, false);
+    const int mode = tma_ring_for(d->bandwidth).mode;
+    int64_t tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, mode);
+    if (tma > kOptin && mode == (int)bwm::kRingTmem)
+        tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, bwm::kRingLag);
+    return tma > 0 ? tma : ldg;
 }
 
 int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_plan** out_plan) {
@@ -437,6 +444,20 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     plan->smem = smem_bytes_for(N, n, h, p, plan->ring);
     plan->tring = tma_ring_for(h);
     plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->tring.mode);
+    {
+        // long series: when the staged tables do not fit, run the lagging-cursor variants,
+        // which read the tables through L1 (any N)
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        if (plan->smem > optin && plan->ring) {
+            plan->ring = false;
+            plan->smem = smem_bytes_for(N, n, h, p, false);
+        }
+        if (plan->smem_tma > optin && plan->tring.mode == (int)bwm::kRingTmem) {
+            plan->tring = {(int)bwm::kRingLag, 0, 0};
+            plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->tring.mode);
+        }
+    }
     const char* env = getenv("BWM_KERNEL");
     plan->force_ldg = env && strcmp(env, "ldg") == 0;
     plan->inv_dof = (float)(1.0 / (double)(n - p));

@@ -41,14 +41,20 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
     constexpr int D = kDepth;
     extern __shared__ __align__(16) float smem[];
     const int N = prm.N, n = prm.n, h = prm.h;
-    float* s_mt = smem;                       // [n][SP]
-    float* s_xt = s_mt + n * SP;              // [N][SP]
-    float* s_bd = s_xt + N * SP;              // [N-n] (padded to 4)
+    // RING: the coefficient tables live in smem.  !RING (large h or long series): they stay
+    // in global memory, read through L1 (uniform addresses), so any N fits; only the
+    // boundary is staged.
+    float* s_tab = smem;
+    const float* s_mt = RING ? s_tab : prm.mt;                                 // [n][SP]
+    const float* s_xt = RING ? s_tab + n * SP : prm.xt;                        // [N][SP]
+    float* s_bd = s_tab + (RING ? (n + N) * SP : 0);                           // [N-n] (padded to 4)
     float2* s_ring = reinterpret_cast<float2*>(s_bd + ((N - n + 3) & ~3));   // [h][kThreads]
 
     // --- constant tables -> smem (once per persistent CTA) -------------------------
-    for (int i = threadIdx.x; i < n * SP; i += kThreads) s_mt[i] = prm.mt[i];
-    for (int i = threadIdx.x; i < N * SP; i += kThreads) s_xt[i] = prm.xt[i];
+    if (RING) {
+        for (int i = threadIdx.x; i < n * SP; i += kThreads) s_tab[i] = prm.mt[i];
+        for (int i = threadIdx.x; i < N * SP; i += kThreads) s_tab[n * SP + i] = prm.xt[i];
+    }
     for (int i = threadIdx.x; i < N - n; i += kThreads) s_bd[i] = prm.bound[i];
     __syncthreads();
 

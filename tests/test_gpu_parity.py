@@ -247,3 +247,24 @@ def test_critical_value_matches_pinned():
     req = pkg.CriticalValueRequest(**pinned["request"])
     lam = pkg.critical_value(req, threads=8)
     assert lam == pytest.approx(pinned["value"], rel=2e-5)
+
+
+@pytest.mark.parametrize("N,n,h,k", [(3000, 1500, 20, 8), (2600, 1300, 400, 6)])
+def test_long_series(N, n, h, k):
+    """Series too long for shared-memory tables (N * p floats > 227 KB): the lagging-cursor
+    kernels read their tables through L1 — any N is supported, as in the reference."""
+    pkg = _pkg()
+    from paper_1807_01751_b200.synth import host_stack
+
+    t = np.cumsum(np.random.default_rng(3).uniform(1, 9, N)) + 1.0
+    y = host_stack(1500, t, 365.25, n, 0.3, seed=11)
+    crit = 3.0
+    cfg = pkg.MonitorConfig(history=n, bandwidth=h, harmonics=k, freq=365.25, crit_value=crit)
+    bm = pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+    ref = bo.monitor(y, t, n, h, k, 365.25, crit, keep_mosum=True)
+    assert np.array_equal(bm.valid, ref.valid)
+    first_gpu = np.where(bm.first_break > 0, bm.first_break - n, 0)
+    pairs = bo.near_pairs(ref.mosum, bo.boundary(n, N, crit))
+    border = bo.borderline_from_pairs(pairs, N - n, y.shape[1], ref.first_idx, first_gpu)
+    assert not np.any((first_gpu != ref.first_idx) & ~border & ref.valid)
+    np.testing.assert_allclose(bm.max_abs_mo[ref.valid], ref.max_abs_mo[ref.valid], rtol=RTOL, atol=0)
