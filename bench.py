@@ -44,7 +44,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C4", "C5"])
+    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"],
+                    help="C2 (default): every rank runs a 4096^2 stack (weak scaling); C3: the "
+                         "16384^2 scene split into one pixel band per rank (strong scaling, N >= 2)")
     ap.add_argument("--nan-mode", default="fill", choices=["fill", "mask"],
                     help="fill: the reference's gap fill (headline); mask: per-pixel masked fits (extension)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -220,6 +222,29 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def h2d_link_gbs(host, nbytes: int = 1 << 30) -> float:
+    """Measured pinned host -> device copy rate (GB/s): two nbytes halves on two streams."""
+    import torch
+
+    flat = host.view(-1).view(torch.uint8)[: 2 * nbytes]
+    dev = torch.empty(2 * nbytes, dtype=torch.uint8, device="cuda")
+    streams = [torch.cuda.Stream() for _ in range(2)]
+
+    def once():
+        for i, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                dev[i * nbytes:(i + 1) * nbytes].copy_(flat[i * nbytes:(i + 1) * nbytes], non_blocking=True)
+        torch.cuda.synchronize()
+
+    once()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        once()
+    dt = time.perf_counter() - t0
+    del dev
+    return 3 * 2 * nbytes / dt / 1e9
+
+
 def e2e_file(ynp, t, cfg, steps, world):
     """monitor_file on a BTS1 file of the same stack (dataio.monitor_file -> bwm_monitor_file):
     file read (page cache) + H2D + kernel + D2H; the file lives in /dev/shm (RAM) when it fits."""
@@ -272,6 +297,14 @@ def run_ours(args):
     w = WORKLOADS[args.workload]
     t = time_axis(w)
     P = w.n_pixels
+    strong = args.workload == "C3"
+    if strong:                                   # one 16-byte-aligned pixel band of the scene per rank
+        from paper_1807_01751_b200.sharding import shard_bounds
+
+        a, b = shard_bounds(w.n_pixels, world, align=256)[rank]
+        P = b - a
+        if P * w.n_obs * 4 > 0.9 * torch.cuda.get_device_properties(dev).total_memory:
+            raise SystemExit(f"C3 needs more ranks: {P * w.n_obs * 4 / 1e9:.0f} GB per rank")
     plan = DevicePlan(TimeAxis(t), w.freq, w.harmonics, w.n_hist, w.bandwidth, w.crit, dev, nan_mode=args.nan_mode)
     y = device_stack(P, t, w.freq, w.n_hist, w.nan_frac, seed=20261017 + rank, device=dev)
     torch.cuda.synchronize()
@@ -306,7 +339,8 @@ def run_ours(args):
     kernel_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     k_avg = sum(kernel_ms) / len(kernel_ms)
     ms_per_step = elapsed_ms / args.steps
-    value = world * P / (ms_per_step * 1e-3) / 1e6
+    total_px = w.n_pixels if strong else world * P
+    value = total_px / (ms_per_step * 1e-3) / 1e6
     peak, peak_kind = peaks()
     bpp = bytes_per_pixel(w)
     achieved = P * bpp / (k_avg * 1e-3) / 1e9
@@ -360,6 +394,11 @@ def run_ours(args):
                        "stack, one kernel launch, device-side finalize to the reference dtypes, D2H of "
                        "valid/detected/first_break(int64)/max_abs_mo(float64)"}
         assert bm.break_count > 0
+        # the e2e roofline: this box's pinned H2D link rate (two 1 GiB copies on two streams,
+        # the way bwm_monitor_host splits the stack) against the stack bytes per step
+        link = h2d_link_gbs(host)
+        e2e["h2d_link_gbs"] = link
+        e2e["h2d_link_frac"] = ynp.nbytes / (e2e["ms_per_step"] * 1e-3) / 1e9 / link
         if args.e2e_file:
             e2e["file"] = e2e_file(ynp, t, cfg, args.e2e_steps, world)
 
@@ -387,13 +426,15 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic NDVI-like stack generated in HBM (torch Philox), seed 20261017+rank",
-            "config": {"workload": f"{w.name}: {w.rows}x{w.cols} px per GPU, N={w.n_obs} dates, n={w.n_hist}, "
+            "config": {"workload": f"{w.name}: {w.rows}x{w.cols} px " + (f"split over {world} GPUs" if strong else "per GPU")
+                                   + f", N={w.n_obs} dates, n={w.n_hist}, "
                                    f"k={w.harmonics}, h={w.bandwidth}, {int(w.nan_frac * 100)}% NaN",
                        "nan_mode": args.nan_mode,
-                       "pixels_total": world * P, "lambda": w.crit,
+                       "pixels_total": total_px, "pixels_per_rank": P, "lambda": w.crit,
                        "l2": f"input {w.n_obs * P * 4 / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush needed)",
                        "parallelism": f"pixel tiles, {world} rank(s), no collective on the data path"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
