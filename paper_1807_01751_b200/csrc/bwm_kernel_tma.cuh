@@ -275,7 +275,10 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
     const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(wu * 32) << 16) : 0u;
     auto tcol = [&](int row) -> uint32_t { return tbase + (uint32_t)(2 * row); };
     // ring row q of time t is t mod L (2 columns per row: 2L columns, no mirror rows)
-    auto ring_put = [&](int t, float2 v) { tmem_st2(tcol(t % L), v); };
+    // ring rows of the fixed dates of every tile (one modulo each, per CTA)
+    const int q_w0 = MODE == kRingTmem ? w0 % L : 0, q_wstart = MODE == kRingTmem ? wstart % L : 0;
+    const int q_t3 = MODE == kRingTmem ? t3 % L : 0, q_t3h = MODE == kRingTmem ? ((t3 - h) % L + L) % L : 0;
+    const int q_nh = MODE == kRingTmem ? (n - h) % L : 0;
     auto ring_put_row = [&](int q, float2 v) { tmem_st2(tcol(q), v); };   // q < L
     auto ring_ld2 = [&](int q, float2& v) {                                // no wait
         uint32_t a, b;
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
         bool f0 = false, f1 = false;
         float2 last = f2(0.f, 0.f), lastw = f2(0.f, 0.f);
         float2 negc = f2(0.f, 0.f);
+        int pr = q_w0;                                    // ring row of the next parked stage
         for (int t0 = 0; t0 < n; t0 += R) {
             const float2* st = acquire();
             if (t0 == 0) {
@@ -373,18 +377,19 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
                     axpy_row<NP, SP>(part, vc, mrow + k * SP);
                     qpart = fma2(vc, vc, qpart);
                 }
-                if (park) ring_store(t0 % L, yy);
+                if (park) ring_store(pr, yy);
             } else {                                            // last stage: dates [t0, n) only
 #pragma unroll 1
                 for (int k = 0; k < n - t0; ++k) {
                     const float2 vc = fill(st[k * ROWF2], negc, last);
-                    if (park) ring_put_row((t0 + k) % L, vc);
+                    if (park) ring_put_row(pr + k >= L ? pr + k - L : pr + k, vc);
                     axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
                     qpart = fma2(vc, vc, qpart);
                 }
             }
             release();
             if (t0 + R == w0) lastw = last;                 // fill state entering pass 2
+            if (park) { pr += R; if (pr >= L) pr -= L; }
             if (((t0 + R) & (kComp - 1)) == 0 || t0 + R >= n) {
 #pragma unroll
                 for (int i = 0; i < NP; ++i) { two_sum(hi[i], lo[i], part[i]); part[i] = f2(0.f, 0.f); }
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
             // the residuals r = y - z^T beta_Q, summing window 0 in date order — the arithmetic
             // of a re-read pass, without re-reading.  R rows per batch, one .x2 access per row.
             tmem_wait_st();
-            int q = wstart % L;
+            int q = q_wstart;
 #pragma unroll 1
             for (int t0 = wstart; t0 < n; t0 += R) {
                 float2 v[R];
@@ -469,7 +474,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
             release();
             if (MODE == kRingTmem) { wb += R; if (wb == L) wb = 0; }
         }
-        if (MODE == kRingTmem) ring_put(n - h, f2(0.f, 0.f));    // r_{n-h} is not in window 0
+        if (MODE == kRingTmem) ring_put_row(q_nh, f2(0.f, 0.f));  // r_{n-h} is not in window 0
 
         // ---- pass 3: monitoring period, fused MOSUM + detect (unscaled frame) ----------
         float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f);
@@ -491,8 +496,8 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
                 if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)(t - n) * prm.ld_out + px0) = mul2(acc, inv);
             }
         };
-        wb = MODE == kRingTmem ? t3 % L : 0;
-        int rb = MODE == kRingTmem ? ((t3 - h) % L + L) % L : 0;   // ring row of t0 - h
+        wb = q_t3;
+        int rb = q_t3h;                                  // ring row of t0 - h
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
             const float2* lst = st + kBoxBytes / 8;      // lag dates (kRingLag): second box
