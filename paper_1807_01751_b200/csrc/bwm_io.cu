@@ -126,9 +126,30 @@ int StagedReader::ensure(int slots, int64_t slot_bytes, std::string* err) {
     return BWM_OK;
 }
 
+void HostSource::copy_rect(const Rect& r, float* dst) const {
+    const int64_t w = r.c1 - r.c0;
+    if (w == ld) {                                          // whole rows: one contiguous block
+        std::memcpy(dst, base + r.r0 * ld, (size_t)((r.r1 - r.r0) * w * 4));
+        return;
+    }
+    for (int64_t t = r.r0; t < r.r1; ++t) std::memcpy(dst + (t - r.r0) * w, base + t * ld + r.c0, (size_t)w * 4);
+}
+
+int StagedReader::start(const HostSource* h, const std::vector<Rect>* rects, int threads) {
+    stop();
+    f_ = nullptr;
+    h_ = h;
+    return launch(rects, threads);
+}
+
 int StagedReader::start(const PayloadFile* f, const std::vector<Rect>* rects, int threads) {
     stop();
     f_ = f;
+    h_ = nullptr;
+    return launch(rects, threads);
+}
+
+int StagedReader::launch(const std::vector<Rect>* rects, int threads) {
     rects_ = rects;
     next_ = 0;
     released_ = 0;
@@ -151,7 +172,11 @@ void StagedReader::worker() {
             if (abort_) return;
         }
         std::string e;
-        const int rc = f_->read_rect((*rects_)[g], slot_[g % K], 1, &e);
+        int rc = BWM_OK;
+        if (h_)
+            h_->copy_rect((*rects_)[g], slot_[g % K]);
+        else
+            rc = f_->read_rect((*rects_)[g], slot_[g % K], 1, &e);
         std::lock_guard<std::mutex> lk(mu_);
         if (rc != BWM_OK) {
             failed_ = abort_ = true;

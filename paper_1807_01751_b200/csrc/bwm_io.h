@@ -41,6 +41,14 @@ struct PayloadFile {
     ~PayloadFile() { close(); }
 };
 
+// A pageable host array [n_obs][ld] (a plain numpy stack): rectangles are memcpy'd into the
+// pinned slots instead of being DMA'd from pageable memory through the driver's bounce buffer.
+struct HostSource {
+    const float* base = nullptr;
+    int64_t ld = 0;
+    void copy_rect(const Rect& r, float* dst) const;
+};
+
 // Rectangles of at most `slot_bytes` covering pixels [c0, c1) x all rows, whole rows first.
 void plan_rects(int64_t n_obs, int64_t c0, int64_t c1, int64_t chunk, int64_t slot_bytes, std::vector<Rect>* out);
 
@@ -50,6 +58,7 @@ class StagedReader {
     // rectangles.  Slots are allocated once and reused across calls.
     int ensure(int slots, int64_t slot_bytes, std::string* err);
     int start(const PayloadFile* f, const std::vector<Rect>* rects, int threads);
+    int start(const HostSource* h, const std::vector<Rect>* rects, int threads);
     // blocks until rectangle g is in its slot; nullptr on a read error (see error()).
     const float* wait(int64_t g);
     // slot of rectangle g may be refilled (its H2D copy has completed)
@@ -60,8 +69,10 @@ class StagedReader {
     ~StagedReader();
 
   private:
+    int launch(const std::vector<Rect>* rects, int threads);
     void worker();
     const PayloadFile* f_ = nullptr;
+    const HostSource* h_ = nullptr;
     const std::vector<Rect>* rects_ = nullptr;
     std::vector<float*> slot_;
     int64_t slot_bytes_ = 0;

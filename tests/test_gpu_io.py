@@ -84,3 +84,25 @@ def test_profile_file_phases(tmp_path):
     bm, t = pkg.profile_file(path, config_for(case))
     assert len(bm) == case.y.shape[1]
     assert t.mosum > 0 and t.ingest > 0 and t.total >= t.mosum
+
+
+@pytest.mark.parametrize("env", [{}, {"BWM_HOST_CHUNK": "3000"}, {"BWM_IO_SLOT_BYTES": "4096"},
+                                 {"BWM_HOST_STAGED": "0"}])
+def test_pageable_host_stack(monkeypatch, env):
+    """A plain (pageable) numpy stack goes through the staged pinned-slot pipeline; the maps
+    equal those of a pinned copy and of the device path, bit for bit."""
+    import torch
+
+    pkg = _pkg()
+    case = load("c1")
+    y = np.ascontiguousarray(case.y[:, :9001])
+    cfg = config_for(case)
+    pinned = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[...] = y
+    ref = pkg.monitor_batch(pkg.SeriesStack(pinned.numpy(), pkg.TimeAxis(case.t)), cfg, return_beta=True)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(case.t)), cfg, return_beta=True)
+    _same(got, ref)
+    dev = pkg.monitor_batch(pkg.SeriesStack(torch.as_tensor(y, device="cuda"), pkg.TimeAxis(case.t)), cfg)
+    _same(dev, pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(case.t)), cfg))
