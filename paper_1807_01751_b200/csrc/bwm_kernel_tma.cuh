@@ -12,13 +12,15 @@
 // Row stream per tile (the issue cursor runs kStages ahead across passes and tiles):
 //   pass 1 : rows [0, n)             beta_Q = Q^T (y - c) and ||y - c||^2 in ONE sweep
 //                                    (pass 0 scans the first stage for c); sigma follows from
-//                                    RSS = ||y-c||^2 - ||beta_Q||^2 (orthonormal basis Q)
-//   pass 2 : rows [w0, n)            the last ~h history rows again (L2 hit): residuals of
-//                                    MOSUM window 0 into the ring, w0 = 8*floor((n-h+1)/8)
+//                                    RSS = ||y-c||^2 - ||beta_Q||^2 (orthonormal basis Q).
+//                                    TMEM mode also parks the filled dates [w0, n) in the ring;
+//                                    once beta is known they become the window-0 residuals
+//                                    in place (no re-read), w0 = 8*floor((n-h+1)/8)
+//   pass 2 : rows [w0, n)            LAG mode only: the window-0 rows again (L2 hits)
 //   pass 3 : rows [8*floor(n/8), N)  MOSUM recurrence + detect (stages 8-date aligned);
 //            LAG mode: each stage also carries dates t-h (second box; t-h < 0 is OOB zero fill)
 // Measured (profiles/probe): SM-side ingest, DRAM or L2, saturates near 7 TB/s, so re-reading
-// the whole history (342 rows/tile) cost ~1 ms at C2; this stream is 266 rows/tile.
+// the whole history (342 rows/tile) cost ~1 ms at C2; the TMEM-mode stream is 232 rows/tile.
 //
 // MOSUM residual ring (r_{t-h} for the add-one/drop-one recurrence, _kernels.py:31-34):
 //   MODE kRingTmem : in Tensor Memory.  Each thread owns its TMEM lane; ring row q of the
@@ -416,7 +418,6 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
         // ---- window 0 ------------------------------------------------------------------
         float2 acc = f2(0.f, 0.f);
         float2 lag_last = w0 == wstart ? lastw : f2(0.f, 0.f);   // kRingLag: fill state at wstart-1
-        int wb = 0;
         if (MODE == kRingTmem) {
             // The ring rows of the dates [wstart, n) (row = date mod L, written in pass 1; h - 1
             // < L rows, so none was overwritten) hold the filled values: convert them in place to
@@ -449,30 +450,24 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
         for (int t0 = w0; MODE == kRingLag && t0 < n; t0 += R) {
             const float2* st = acquire();
             if (t0 + R <= n) {
-                float2 rr[R];
                 const float* xrow = s_xt + t0 * SP;
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const int t = t0 + k;
                     const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), xrow + k * SP, nb);
-                    rr[k] = r;
                     if (t >= wstart) acc = add2(acc, r);
-                    if (MODE == kRingLag && t == wstart - 1) lag_last = last;
+                    if (t == wstart - 1) lag_last = last;
                 }
-                if (MODE == kRingTmem) ring_store(wb, rr);
             } else {                                            // last stage: dates [t0, n) only
-                if (MODE == kRingTmem) tmem_wait_st();
 #pragma unroll 1
                 for (int k = 0; k < n - t0; ++k) {
                     const int t = t0 + k;
                     const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                    if (MODE == kRingTmem) ring_put_row(wb + k, r);
                     if (t >= wstart) acc = add2(acc, r);
-                    if (MODE == kRingLag && t == wstart - 1) lag_last = last;
+                    if (t == wstart - 1) lag_last = last;
                 }
             }
             release();
-            if (MODE == kRingTmem) { wb += R; if (wb == L) wb = 0; }
         }
         if (MODE == kRingTmem) ring_put_row(q_nh, f2(0.f, 0.f));  // r_{n-h} is not in window 0
 
@@ -496,7 +491,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
                 if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)(t - n) * prm.ld_out + px0) = mul2(acc, inv);
             }
         };
-        wb = q_t3;
+        int wb = q_t3;                                   // ring row of t0
         int rb = q_t3h;                                  // ring row of t0 - h
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
