@@ -45,6 +45,9 @@ namespace bwm {
 constexpr int kMaskThreads = 128;       // one pixel per thread; M = 128 of the Gram MMA
 constexpr int kMaskTile = kMaskThreads;
 constexpr int kMaskD = 16;              // dates per register block = 2 MMA K-steps
+#ifndef BWM_MASK_D23
+#define BWM_MASK_D23 16
+#endif
 constexpr int kMaskBStages = 4;         // x x^T tile ring: refilled 2 blocks behind, 2 ahead
 constexpr int kMaskABufs = 4;           // TMEM A buffers (16 columns each)
 
@@ -142,6 +145,7 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
     constexpr int SP = Coefs<NP>::SP;
     constexpr int KK = Gram<NP>::KK, NN = Gram<NP>::NN, SB = Gram<NP>::SB;
     constexpr int D = kMaskD, S = kMaskBStages, AB = kMaskABufs;
+    constexpr int D23 = BWM_MASK_D23;   // dates per register block of passes 2 and 3 (8: C2 -3%, C5 +7%, C4 +60%)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
     const int n16 = ((n + D - 1) / D) * D;
@@ -204,16 +208,17 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
         // 12.1 ms at C2; two blocks ahead measured slower).
         const float* wp = prm.y + tile * kMaskTile + 32 * warp;
         const bool pf_ok = tile * kMaskTile + 32 * warp + 31 < prm.n_pixels;
-        auto load = [&](int t0, int end, float (&vb)[D]) {
-            if (pf_ok && (tid & 31) < D && t0 + D + (tid & 31) < end)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + (int64_t)(t0 + D + (tid & 31)) * ld));
+        auto load = [&](int t0, int end, auto& vb) {
+            constexpr int DB = (int)(sizeof(vb) / sizeof(float));
+            if (pf_ok && (tid & 31) < DB && t0 + DB + (tid & 31) < end)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + (int64_t)(t0 + DB + (tid & 31)) * ld));
             const float* p = yp + (int64_t)t0 * ldl;
-            if (t0 + D <= end) {
+            if (t0 + DB <= end) {
 #pragma unroll
-                for (int k = 0; k < D; ++k) vb[k] = __ldg(p + k * ldl);
+                for (int k = 0; k < DB; ++k) vb[k] = __ldg(p + k * ldl);
             } else {
 #pragma unroll
-                for (int k = 0; k < D; ++k) vb[k] = t0 + k < end ? __ldg(p + k * ldl) : qnan;
+                for (int k = 0; k < DB; ++k) vb[k] = t0 + k < end ? __ldg(p + k * ldl) : qnan;
             }
         };
 
@@ -349,12 +354,12 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
 #pragma unroll
         for (int i = 0; i < NP / 2; ++i) e2[i] = f2(0.f, 0.f);
         if (hv >= 1) ring[0] = 0.f;              // the element before window 0
-        for (int t0 = 0; t0 < n; t0 += D) {
-            float vb[D];
+        for (int t0 = 0; t0 < n; t0 += D23) {
+            float vb[D23];
             load(t0, n, vb);
             float part = 0.f;
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
+            for (int k = 0; k < D23; ++k) {
                 const int t = t0 + k;
                 const bool m = finitef(vb[k]);
                 const float r = resid(m ? vb[k] - c : 0.f, t);
@@ -438,12 +443,12 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
         const int64_t ld_out = prm.ld_out;
         // log_plus(x) = 1 while x = (n_v + 1 + j) / n_v <= e, i.e. j < je: b_j = lambda exactly
         const int je = fit_ok ? (int)floorf(1.718281828f * (float)nv - 1.f) + 1 : 0x3fffffff;
-        for (int t0 = n; t0 < N; t0 += D) {
-            float vb[D];
+        for (int t0 = n; t0 < N; t0 += D23) {
+            float vb[D23];
             load(t0, N, vb);
-            const bool slow = __any_sync(0xffffffffu, j + D > je);   // warp-uniform
+            const bool slow = __any_sync(0xffffffffu, j + D23 > je);   // warp-uniform
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
+            for (int k = 0; k < D23; ++k) {
                 const int t = t0 + k;
                 const bool m = finitef(vb[k]) && fit_ok;
                 const float r = resid(m ? vb[k] - c : 0.f, t);
