@@ -346,7 +346,8 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
         delete plan;
         return set_err(BWM_E_DIMS, "masked mode supports at most 65535 dates");
     }
-    std::vector<float> xt((size_t)N * sp, 0.f), tiles((size_t)(n16 / bwm::kMaskD) * nn * 32, 0.f);
+    // X'^T zero-padded by kMaskD rows (the BIG kernel reads it from global memory)
+    std::vector<float> xt((size_t)(N + bwm::kMaskD) * sp, 0.f), tiles((size_t)(n16 / bwm::kMaskD) * nn * 32, 0.f);
     std::vector<double> gf((size_t)kk, 0.0);
     for (int t = 0; t < N; ++t)
         for (int i = 0; i < p; ++i) xt[(size_t)t * sp + i] = (float)tb->design[(size_t)i * N + t];

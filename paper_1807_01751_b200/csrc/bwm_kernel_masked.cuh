@@ -106,7 +106,8 @@ __host__ __device__ inline int masked_scratch_words(int h, int p) { return h + (
 // Shared-memory bytes of the masked kernel (host mirror in bwm_capi.cu).
 __host__ __device__ inline int64_t masked_smem_bytes(int N, int n, int h, int p, bool big) {
     const int sp = (p + 3) & ~3;
-    int64_t bytes = (((int64_t)(N + kMaskD) * sp * 4 + 127) / 128) * 128;   // X'^T, zero rows past N
+    // X'^T with zero rows past N; in BIG mode it stays in global memory (read through L1)
+    int64_t bytes = big ? 0 : (((int64_t)(N + kMaskD) * sp * 4 + 127) / 128) * 128;
     bytes += (int64_t)kMaskBStages * gram_nn(p) * 128;                      // x x^T tile ring
     if (!big) bytes += (int64_t)masked_scratch_words(h, p) * kMaskThreads * 4;
     return bytes + (2 * kMaskBStages + kMaskABufs) * 8 + 16;                // mbarriers + TMEM slot
@@ -150,8 +151,11 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
     const int N = prm.N, n = prm.n, h = prm.h;
     const int n16 = ((n + D - 1) / D) * D;
     const int nkb = n16 / D;                                           // 16-date blocks of the history
-    float* s_x = reinterpret_cast<float*>(smem_raw);                   // [N + D][SP]   X'^T
-    unsigned char* s_b = smem_raw + (((N + D) * SP * 4 + 127) / 128) * 128;   // [S][SB] x x^T tiles
+    // [N + D][SP] X'^T, zero rows past N: staged in smem, or (BIG) read through L1 from the
+    // zero-padded global copy, so the big geometries (C4) fit two CTAs per SM
+    float* s_xs = reinterpret_cast<float*>(smem_raw);
+    const float* s_x = BIG ? prm.xt : s_xs;
+    unsigned char* s_b = smem_raw + (BIG ? 0 : (((N + D) * SP * 4 + 127) / 128) * 128);   // [S][SB] x x^T tiles
     float* s_ring = reinterpret_cast<float*>(s_b + S * SB);           // ring scratch   (!BIG)
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(s_ring) +
                                                   (BIG ? 0 : masked_scratch_words(h, NP) * kMaskThreads * 4));
@@ -160,7 +164,8 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
     uint64_t* m_done = s_bar + 2 * S;      // [AB] MMAs reading A buffer b are done
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * S + AB);
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int i = tid; i < (N + D) * SP; i += kMaskThreads) s_x[i] = i < N * SP ? prm.xt[i] : 0.f;
+    if (!BIG)
+        for (int i = tid; i < (N + D) * SP; i += kMaskThreads) s_xs[i] = i < N * SP ? prm.xt[i] : 0.f;
     if (tid == 0) {
         for (int i = 0; i < 2 * S + AB; ++i) mbar_init(s_bar + i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
