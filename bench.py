@@ -384,8 +384,7 @@ def run_ours(args):
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            bm = None                           # streaming use: the previous map is released first,
-            bm = monitor_batch(stack, cfg)      # so its pinned output blocks are reused
+            bm = monitor_batch(stack, cfg)
         dt = max_over_ranks(time.perf_counter() - t0, world)
         e2e = {"value": world * P * args.e2e_steps / dt / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": int(ynp.nbytes), "d2h_bytes_per_step": int(P * 18 + 16),

@@ -228,6 +228,10 @@ struct HostPipe {
     cudaStream_t s_k[2] = {nullptr, nullptr};
     cudaEvent_t ev_in[2], ev_k0[2], ev_k1[2], ev_free[2];
     bool events = false;
+    // pinned landing zone for result maps whose destination is pageable (plain numpy): the D2H
+    // lands here at full rate and threads memcpy it out (grown on demand, kept across calls)
+    char* h_stage = nullptr;
+    size_t h_stage_bytes = 0;
     double last_kernel_ms = 0, last_total_ms = 0;
     int64_t last_h2d = 0, last_d2h = 0;
 };
@@ -613,6 +617,7 @@ static void pipe_free(HostPipe& hp) {
         }
     }
     cudaFree(hp.d_zero);
+    if (hp.h_stage) cudaFreeHost(hp.h_stage);
     hp = HostPipe();
 }
 
@@ -896,6 +901,38 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
         }
     } reader_guard{reader, slot_ev};
     int64_t h2d = 0, d2h = 0;
+    // result maps: pinned destinations get the D2H directly, pageable ones through the landing zone
+    struct MapDst {
+        void* dst;
+        int elem;
+        size_t off;       // offset of this map in the landing zone (pageable destinations)
+        bool pageable;
+    };
+    auto is_pageable = [](const void* q) {
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, q) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        return !pinned;
+    };
+    MapDst maps[7] = {{out->valid, 1, 0, false},       {out->first_idx, 4, 0, false}, {out->max_abs, 4, 0, false},
+                      {out->first_break, 8, 0, false}, {out->max_abs_f64, 8, 0, false}, {out->detected, 1, 0, false},
+                      {out->mo_mean, 4, 0, false}};
+    size_t stage_need = 0;
+    for (auto& m : maps) {
+        if (!m.dst) continue;
+        m.pageable = is_pageable(m.dst);
+        if (m.pageable) {
+            m.off = stage_need;
+            stage_need += (((size_t)n_pixels * m.elem) + 255) & ~(size_t)255;
+        }
+    }
+    if (stage_need > hp.h_stage_bytes) {
+        if (hp.h_stage) cudaFreeHost(hp.h_stage);
+        hp.h_stage = nullptr;
+        hp.h_stage_bytes = 0;
+        BWM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hp.h_stage), stage_need, cudaHostAllocPortable));
+        hp.h_stage_bytes = stage_need;
+    }
     std::vector<cudaEvent_t> kev((size_t)(2 * n_chunks), nullptr);   // per-chunk kernel timing
     for (auto& ev : kev) BWM_CUDA(cudaEventCreate(&ev));
     for (int64_t c = 0; c < n_chunks; ++c) {
@@ -966,18 +1003,20 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
         rc = bwm_monitor(plan, hp.d_y[b], w, w, pixel_offset + p0, &o, s);
         if (rc) return rc;
         BWM_CUDA(cudaEventRecord(kev[2 * c + 1], s));
-        auto d2h_copy = [&](void* dst, const void* src, size_t bytes) -> int {
+        auto d2h_map = [&](int mi, const void* src) -> int {
+            const MapDst& m = maps[mi];
+            if (!m.dst) return BWM_OK;
+            const size_t bytes = (size_t)w * m.elem;
+            char* dst = m.pageable ? hp.h_stage + m.off + (size_t)p0 * m.elem
+                                   : static_cast<char*>(m.dst) + (size_t)p0 * m.elem;
             BWM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
             d2h += (int64_t)bytes;
             return BWM_OK;
         };
-        if ((rc = d2h_copy(out->valid + p0, hp.d_valid[b], (size_t)w))) return rc;
-        if (out->first_idx && (rc = d2h_copy(out->first_idx + p0, hp.d_first[b], (size_t)w * 4))) return rc;
-        if (out->max_abs && (rc = d2h_copy(out->max_abs + p0, hp.d_max[b], (size_t)w * 4))) return rc;
-        if (out->first_break && (rc = d2h_copy(out->first_break + p0, hp.d_fb[b], (size_t)w * 8))) return rc;
-        if (out->max_abs_f64 && (rc = d2h_copy(out->max_abs_f64 + p0, hp.d_mx64[b], (size_t)w * 8))) return rc;
-        if (out->detected && (rc = d2h_copy(out->detected + p0, hp.d_det[b], (size_t)w))) return rc;
-        if (out->mo_mean && (rc = d2h_copy(out->mo_mean + p0, hp.d_mean[b], (size_t)w * 4))) return rc;
+        const void* srcs[7] = {hp.d_valid[b], hp.d_first[b], hp.d_max[b], hp.d_fb[b], hp.d_mx64[b], hp.d_det[b],
+                               hp.d_mean[b]};
+        for (int mi = 0; mi < 7; ++mi)
+            if ((rc = d2h_map(mi, srcs[mi]))) return rc;
         if (out->beta) {
             BWM_CUDA(cudaMemcpy2DAsync(out->beta + p0, (size_t)out->ld_out * 4, hp.d_beta[b], (size_t)w * 4,
                                        (size_t)w * 4, (size_t)p, cudaMemcpyDeviceToHost, s));
@@ -989,6 +1028,27 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
             d2h += w * 4 * M;
         }
         BWM_CUDA(cudaEventRecord(hp.ev_free[b], s));
+    }
+    // while the GPU transfers and computes: touch the pages of the pageable map destinations
+    // (fresh numpy arrays fault on first write), so the copy-out below runs at memory speed
+    {
+        std::vector<std::pair<char*, size_t>> jobs;
+        const size_t piece = 8u << 20;
+        for (const auto& m : maps) {
+            if (!m.dst || !m.pageable) continue;
+            const size_t total = (size_t)n_pixels * m.elem;
+            for (size_t a = 0; a < total; a += piece)
+                jobs.emplace_back(static_cast<char*>(m.dst) + a, std::min(piece, total - a));
+        }
+        const int nt = (int)std::min<size_t>(jobs.size(), std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+        std::atomic<size_t> next{0};
+        auto work = [&]() {
+            for (size_t j; (j = next.fetch_add(1)) < jobs.size();) std::memset(jobs[j].first, 0, jobs[j].second);
+        };
+        std::vector<std::thread> th;
+        for (int i = 1; i < nt; ++i) th.emplace_back(work);
+        if (nt > 0) work();
+        for (auto& t : th) t.join();
     }
     double kernel_ms = 0;
     for (int64_t c = 0; c < n_chunks; ++c) {
@@ -1005,6 +1065,29 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
     for (int b = 0; b < 2; ++b) {
         BWM_CUDA(cudaStreamSynchronize(hp.s_k[b]));
         BWM_CUDA(cudaStreamSynchronize(hp.s_h2d[b]));
+    }
+    {
+        // landing zone -> pageable destinations, split over threads
+        std::vector<std::pair<char*, const char*>> jobs;
+        std::vector<size_t> lens;
+        const size_t piece = 16u << 20;
+        for (const auto& m : maps) {
+            if (!m.dst || !m.pageable) continue;
+            const size_t total = (size_t)n_pixels * m.elem;
+            for (size_t a = 0; a < total; a += piece) {
+                jobs.emplace_back(static_cast<char*>(m.dst) + a, hp.h_stage + m.off + a);
+                lens.push_back(std::min(piece, total - a));
+            }
+        }
+        const int nt = (int)std::min<size_t>(jobs.size(), std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+        std::atomic<size_t> next{0};
+        auto work = [&]() {
+            for (size_t j; (j = next.fetch_add(1)) < jobs.size();) std::memcpy(jobs[j].first, jobs[j].second, lens[j]);
+        };
+        std::vector<std::thread> th;
+        for (int i = 1; i < nt; ++i) th.emplace_back(work);
+        work();
+        for (auto& t : th) t.join();
     }
     int64_t z[2];
     BWM_CUDA(cudaMemcpy(z, hp.d_zero, sizeof z, cudaMemcpyDeviceToHost));

@@ -10,7 +10,7 @@ pkg/src/breakwatch/dataio.py:
 The payload is already the layout the kernel reads, so nothing is transposed or converted:
   read_stack     parses the 17-byte header (and axis) here with the reference's checks and
                  messages (dataio.py:79-115), then reads the payload with libbwm's parallel
-                 pread (bwm_read_payload) into page-locked memory, ready for a full-rate H2D;
+                 pread (bwm_read_payload);
   monitor_file   skips the host copy altogether: libbwm streams row blocks of the payload
                  from the page cache into pinned slots while earlier blocks are already being
                  DMA'd to HBM (bwm_monitor_file), then runs the kernel — the paper's
@@ -125,18 +125,16 @@ def write_stack(stack: SeriesStack, sink) -> int:
 
 
 def _payload_buffer(n_obs: int, n_pixels: int) -> np.ndarray:
-    from .device import _pinned
-
-    return _pinned((n_obs, n_pixels), np.float32)
+    # plain memory: monitor_batch stages pageable stacks through libbwm's pinned slots at the
+    # link rate, and a multi-GB page-locked allocation would cost seconds per file
+    return np.empty((n_obs, n_pixels), np.float32)
 
 
 def read_stack(source, *, threads: Optional[int] = None) -> SeriesStack:
     """Parse a stack from a path or binary file object (dataio.py:79-115).
 
     Malformed input raises StackFormatError (StackCapacityError for a plausible header that
-    declares more than PAYLOAD_LIMIT_BYTES); no partial stack is returned.  The samples land
-    in page-locked memory when a CUDA runtime is present, so monitor_batch's H2D runs at full
-    PCIe rate.
+    declares more than PAYLOAD_LIMIT_BYTES); no partial stack is returned.
     """
     if _is_path(source):
         with open(source, "rb") as handle:

@@ -67,6 +67,12 @@ def _pinned(shape, dtype):
         return np.empty(shape, dtype=dtype)
 
 
+def _host_array(shape, dtype) -> np.ndarray:
+    """Plain (pageable) numpy result array; libbwm touches its pages while the GPU works and
+    copies the maps in from its pinned landing zone (bwm_monitor_host)."""
+    return np.empty(shape, dtype)
+
+
 def _axis_key(axis: TimeAxis) -> str:
     return hashlib.sha1(np.ascontiguousarray(axis.values).tobytes()).hexdigest()
 
@@ -229,18 +235,21 @@ class DevicePlan:
         return self._host_call(call, "bwm_monitor_file", P, keep_mosum, beta, mean, ref_dtypes)
 
     def _host_call(self, call, what, P, keep_mosum, beta, mean, ref_dtypes) -> DeviceResult:
+        # Plain numpy results: libbwm lands the maps in its own pinned zone and copies them out
+        # with threads, so a caller that keeps many BreakMaps does not hoard page-locked memory
+        # (and does not pay a page-locked allocation per call).
         out = DeviceResult(
-            valid=_pinned(P, np.uint8),
-            first_idx=None if ref_dtypes else _pinned(P, np.int32),
-            max_abs=None if ref_dtypes else _pinned(P, np.float32),
-            beta=_pinned((self.n_params, P), np.float32) if beta else None,
-            mo_mean=_pinned(P, np.float32) if mean else None,
-            mosum=_pinned((self.n_obs - self.n_hist, P), np.float32) if keep_mosum else None,
+            valid=_host_array(P, np.uint8),
+            first_idx=None if ref_dtypes else _host_array(P, np.int32),
+            max_abs=None if ref_dtypes else _host_array(P, np.float32),
+            beta=_host_array((self.n_params, P), np.float32) if beta else None,
+            mo_mean=_host_array(P, np.float32) if mean else None,
+            mosum=_host_array((self.n_obs - self.n_hist, P), np.float32) if keep_mosum else None,
         )
         if ref_dtypes:
-            out.first_break = _pinned(P, np.int64)
-            out.max_abs_f64 = _pinned(P, np.float64)
-            out.detected = _pinned(P, np.uint8)
+            out.first_break = _host_array(P, np.int64)
+            out.max_abs_f64 = _host_array(P, np.float64)
+            out.detected = _host_array(P, np.uint8)
         zero = np.array([_lib.INT64_MAX], dtype=np.int64)
         ptr = lambda a: a.ctypes.data if a is not None else None  # noqa: E731
         o = _lib.Outputs(ptr(out.valid), ptr(out.first_idx), ptr(out.max_abs), ptr(out.beta),
