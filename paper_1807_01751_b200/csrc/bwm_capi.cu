@@ -421,8 +421,12 @@ int64_t bwm_smem_bytes(const bwm_dims* d) {
     if (ldg > kOptin && ring) ldg = smem_bytes_for(d->n_obs, d->n_hist, d->bandwidth, d->n_params, false);
     const int mode = tma_ring_for(d->bandwidth).mode;
     int64_t tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, mode);
-    if (tma > kOptin && mode == (int)bwm::kRingTmem)
-        tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, bwm::kRingLag);
+    int tmode = mode;
+    if (tma > kOptin && mode == (int)bwm::kRingTmem) tmode = bwm::kRingLag;
+    if (tmode == (int)bwm::kRingLag &&
+        smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, bwm::kRingLagT) <= (110 << 10))
+        tmode = bwm::kRingLagT;
+    if (tmode != mode) tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, tmode);
     return tma > 0 ? tma : ldg;
 }
 
@@ -460,6 +464,12 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         }
         if (plan->smem_tma > optin && plan->tring.mode == (int)bwm::kRingTmem) {
             plan->tring = {(int)bwm::kRingLag, 0, 0};
+            plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->tring.mode);
+        }
+        // lagging cursor: tables staged in smem when they fit (kRingLagT), else through L1
+        if (plan->tring.mode == (int)bwm::kRingLag &&
+            smem_bytes_tma(N, n, h, p, bwm::kRingLagT) <= std::min<int64_t>(optin, 110 << 10)) {
+            plan->tring = {(int)bwm::kRingLagT, 0, 0};
             plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->tring.mode);
         }
     }

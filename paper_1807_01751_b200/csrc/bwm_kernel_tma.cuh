@@ -28,7 +28,9 @@
 //                    stage height R, >= h), 2L columns (64 at h <= 32, so TMEM admits 8 CTAs
 //                    per SM).  Per stage: R/8 tcgen05.st.x16, and R/8 tcgen05.ld.x16 for the
 //                    lagged rows (R .x2 loads on the stages whose window wraps).
-//   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged date t-h (large h).
+//   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged date t-h (large h); tables
+//                    read through L1 (any series length).  kRingLagT: the same with the tables
+//                    staged in shared memory (when they fit).
 //   (h < R, where an R-row batch would read rows it has not written yet, runs the LDG kernel.)
 //
 // The monitoring pass runs in the UNSCALED frame: acc = sum of window residuals, crossing
@@ -54,14 +56,18 @@ constexpr int kStageRows = BWM_STAGE_ROWS;      // dates per stage (multiple of 
 #endif
 constexpr int kStages = BWM_STAGES;             // stage ring depth per warp (TMEM-ring mode)
 // the lagging-cursor mode moves two boxes per stage (dates t and t-h): 3 stages = 6 boxes
-__host__ __device__ constexpr int stages_for(int mode) { return mode == 2 /* kRingLag */ ? BWM_STAGES_LAG : kStages; }
+// (kRingLag: tables in global memory, 3 stages, 3 CTAs/SM; kRingLagT: tables in smem, 2 stages,
+//  2 CTAs/SM — measured 8.85 vs 8.11 ms at C4, so kRingLagT whenever its tables fit)
+__host__ __device__ constexpr int stages_for(int mode) {
+    return mode == 2 /* kRingLag */ ? BWM_STAGES_LAG : mode == 3 /* kRingLagT */ ? 2 : kStages;
+}
 static_assert(kStageRows == 8 || kStageRows == 16, "stage height: 8 or 16 dates (compensation blocks are 16)");
 constexpr int kWarpPx = 64;                     // pixels per warp slice (32 lanes x 2)
 constexpr int kBoxBytes = kStageRows * kWarpPx * 4;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTmaThreads = kThreads;
 
-enum RingMode { kRingSmem = 0, kRingTmem = 1, kRingLag = 2 };
+enum RingMode { kRingSmem = 0, kRingTmem = 1, kRingLag = 2, kRingLagT = 3 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -170,7 +176,7 @@ __device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
 
 // Shared-memory footprint per warp stage (host mirror in bwm_capi.cu).
 __host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
-    return (int64_t)kBoxBytes * (mode == kRingLag ? 2 : 1);
+    return (int64_t)kBoxBytes * (mode == kRingLag || mode == kRingLagT ? 2 : 1);
 }
 
 #ifndef BWM_TMA_MINB
@@ -184,9 +190,10 @@ __host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
 // for all BASELINE geometries, N/n = 2) — the per-date boundary product, mean accumulation
 // and output branch drop out of the MOSUM loop.  Results are bit-identical to !LEAN.
 template <int NP, int MODE, bool LEAN>
-__global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA_MINB_BIG)
+__global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE == 3 /* kRingLagT */ ? 2 : BWM_TMA_MINB_BIG)
     monitor_kernel_tma(const __grid_constant__ KParams prm) {
-    static_assert(MODE == kRingTmem || MODE == kRingLag, "TMA kernel: TMEM ring or lagging cursor");
+    static_assert(MODE == kRingTmem || MODE == kRingLag || MODE == kRingLagT, "TMA kernel: TMEM ring or lagging cursor");
+    constexpr bool kLag = MODE == kRingLag || MODE == kRingLagT;
     constexpr int SP = Coefs<NP>::SP;
     constexpr int R = kStageRows;
     constexpr int S = stages_for(MODE);
@@ -260,7 +267,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
         if (itile >= n_tiles) return;
         const int r0 = s_rows[istage];
         const uint32_t dst = stage_u32 + (uint32_t)(slot * SB), bar = bar_u32 + (uint32_t)(slot * 8);
-        if (MODE == kRingLag && istage >= st1 + st2)
+        if (kLag && istage >= st1 + st2)
             tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBoxBytes);   // + dates t-h (<0: zero fill)
         else
             tma_box_elect(dst, &prm.tmap, xw, r0, bar, kBoxBytes);
@@ -446,8 +453,8 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
                 q = q + R >= L ? q + R - L : q + R;
             }
         }
-        if (MODE == kRingLag) last = lastw;                     // pass 2 re-reads [w0, n)
-        for (int t0 = w0; MODE == kRingLag && t0 < n; t0 += R) {
+        if (kLag) last = lastw;                                 // pass 2 re-reads [w0, n)
+        for (int t0 = w0; kLag && t0 < n; t0 += R) {
             const float2* st = acquire();
             if (t0 + R <= n) {
                 const float* xrow = s_xt + t0 * SP;
@@ -496,7 +503,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : BWM_TMA
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
             const float2* lst = st + kBoxBytes / 8;      // lag dates (kRingLag): second box
-            if (t0 >= n + (MODE == kRingLag ? 1 : 0) && t0 + R <= N) {
+            if (t0 >= n + (kLag ? 1 : 0) && t0 + R <= N) {
                 float2 oldv[R], newv[R];
                 if (MODE == kRingTmem) ring_load(rb, oldv);
                 float4 b4[R / 4];

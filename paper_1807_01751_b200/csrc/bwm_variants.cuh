@@ -24,10 +24,12 @@ constexpr int kTmaLean = 0x10;   // pick(): OR into the TMA ring mode for the LE
                 return ring ? bwm::monitor_kernel_ldg<NP, true, true> : bwm::monitor_kernel_ldg<NP, true, false>;   \
             default:                                                                             \
                 if (mode & bwm::kTmaLean)                                                        \
-                    return (mode & 0xF) == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem, true> \
-                                                          : bwm::monitor_kernel_tma<NP, bwm::kRingLag, true>; \
-                return (mode & 0xF) == bwm::kRingTmem ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem, false> \
-                                                      : bwm::monitor_kernel_tma<NP, bwm::kRingLag, false>; \
+                    return (mode & 0xF) == bwm::kRingTmem  ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem, true>  \
+                           : (mode & 0xF) == bwm::kRingLagT ? bwm::monitor_kernel_tma<NP, bwm::kRingLagT, true> \
+                                                           : bwm::monitor_kernel_tma<NP, bwm::kRingLag, true>;  \
+                return (mode & 0xF) == bwm::kRingTmem  ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem, false>      \
+                       : (mode & 0xF) == bwm::kRingLagT ? bwm::monitor_kernel_tma<NP, bwm::kRingLagT, false>     \
+                                                       : bwm::monitor_kernel_tma<NP, bwm::kRingLag, false>;      \
         }                                                                                        \
     }
 

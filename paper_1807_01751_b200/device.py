@@ -151,7 +151,7 @@ class DevicePlan:
         pi = _lib.PlanInfo()
         _lib.check(self._lib.bwm_plan_info(self._handle, C.byref(pi)), "bwm_plan_info")
         d = {name: getattr(pi, name) for name, _ in _lib.PlanInfo._fields_}
-        d["ring_mode"] = {-1: "none", 0: "smem", 1: "tmem", 2: "lag"}[d["ring_mode"]]
+        d["ring_mode"] = {-1: "none", 0: "smem", 1: "tmem", 2: "lag", 3: "lag_smem_tables"}[d["ring_mode"]]
         d["nan_mode"] = {v: k for k, v in _lib.NAN_MODES.items()}[d["nan_mode"]]
         return d
 
