@@ -1,0 +1,67 @@
+"""Seeded random geometries through the whole GPU path against the float64 oracle.
+
+Covers the rarely hit corners in one sweep: every kernel mode (TMEM ring with and without
+wrapping lag windows, both lagging-cursor modes, the LDG kernels for h < 8 and the tail tile),
+harmonic orders 1-8, regular and irregular axes, pixel counts that are not multiples of a
+tile, NaN fractions from none to most, monitoring horizons up to 4x the history.
+Tolerances as in test_gpu_parity.py.
+"""
+import numpy as np
+import pytest
+
+from oracle import bfast_oracle as bo
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+
+
+def _geometries(count=20, seed=20261017):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(count):
+        k = int(rng.integers(1, 9))
+        p = 2 + 2 * k
+        N = int(rng.integers(max(40, 3 * p), 420))
+        # monitoring horizons up to 4x the history (the float32 trend extrapolation
+        # error grows with N/n; the BASELINE geometries use N/n = 2)
+        n = int(rng.integers(max(p + 4, (N + 3) // 4), N - 4))
+        h = int(rng.choice([int(rng.integers(1, 8)), int(rng.integers(8, 40)), int(rng.integers(1, n + 1))]))
+        h = max(1, min(h, n))
+        P = int(rng.integers(1, 3000))
+        nan = float(rng.choice([0.0, 0.2, 0.6]))
+        irregular = bool(rng.integers(0, 2))
+        out.append((i, N, n, h, k, P, nan, irregular))
+    return out
+
+
+@pytest.mark.parametrize("i,N,n,h,k,P,nan,irregular", _geometries())
+def test_random_geometry(i, N, n, h, k, P, nan, irregular):
+    import paper_1807_01751_b200 as pkg
+    from paper_1807_01751_b200.synth import host_stack
+
+    rng = np.random.default_rng(100 + i)
+    t = np.cumsum(rng.uniform(1, 9, N)) + 1.0 if irregular else np.arange(1.0, N + 1.0)
+    freq = 365.25 if irregular else 23.0
+    y = host_stack(P, t, freq, n, nan, seed=200 + i)
+    crit = 3.0
+    cfg = pkg.MonitorConfig(history=n, bandwidth=h, harmonics=k, freq=freq, crit_value=crit)
+    try:
+        ref = bo.monitor(y, t, n, h, k, freq, crit, keep_mosum=True)
+    except Exception as exc:                      # geometry the reference rejects: so must we
+        want = (pkg.ZeroResidualError if isinstance(exc, bo.OracleZeroResidual)
+                else pkg.RankDeficiencyError if "rank deficient" in str(exc) else type(exc))
+        with pytest.raises(want):
+            pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+        return
+    bm = pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+    assert np.array_equal(bm.valid, ref.valid)
+    first_gpu = np.where(bm.first_break > 0, bm.first_break - n, 0)
+    pairs = bo.near_pairs(ref.mosum, bo.boundary(n, N, crit))
+    border = bo.borderline_from_pairs(pairs, N - n, P, ref.first_idx, first_gpu)
+    filled, _ = bo.fill_block(y)
+    degen = (filled[:n] == filled[0]).all(axis=0)
+    bad = np.flatnonzero((first_gpu != ref.first_idx) & ~border & ~degen & ref.valid)
+    assert bad.size == 0, f"{bad.size} mismatches, e.g. {bad[:5]}"
+    ok = ref.valid & ~degen
+    np.testing.assert_allclose(bm.max_abs_mo[ok], ref.max_abs_mo[ok], rtol=RTOL, atol=0)
