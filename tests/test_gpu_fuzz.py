@@ -65,3 +65,33 @@ def test_random_geometry(i, N, n, h, k, P, nan, irregular):
     assert bad.size == 0, f"{bad.size} mismatches, e.g. {bad[:5]}"
     ok = ref.valid & ~degen
     np.testing.assert_allclose(bm.max_abs_mo[ok], ref.max_abs_mo[ok], rtol=RTOL, atol=0)
+
+
+@pytest.mark.parametrize("i,N,n,h,k,P,nan,irregular", _geometries(count=10, seed=7))
+def test_random_geometry_masked(i, N, n, h, k, P, nan, irregular):
+    """The same sweep in nan_mode="mask" against the per-pixel masked oracle (600 px each)."""
+    import paper_1807_01751_b200 as pkg
+    from paper_1807_01751_b200.synth import host_stack
+
+    P = min(P, 600)
+    rng = np.random.default_rng(300 + i)
+    t = np.cumsum(rng.uniform(1, 9, N)) + 1.0 if irregular else np.arange(1.0, N + 1.0)
+    freq = 365.25 if irregular else 23.0
+    y = host_stack(P, t, freq, n, nan, seed=400 + i)
+    crit = 3.0
+    cfg = pkg.MonitorConfig(history=n, bandwidth=h, harmonics=k, freq=freq, crit_value=crit, nan_mode="mask")
+    try:
+        ref = bo.monitor_masked(y, t, n, h, k, freq, crit)
+    except bo.OracleZeroResidual:
+        with pytest.raises(pkg.ZeroResidualError):
+            pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+        return
+    try:
+        bm = pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+    except pkg.RankDeficiencyError:
+        pytest.skip("full-history design rank deficient (checked before any pixel is fitted)")
+    assert np.array_equal(bm.valid, ref.valid)
+    bad = np.flatnonzero((bm.first_break != ref.first_break) & ~ref.near & ref.valid)
+    assert bad.size == 0, f"{bad.size} mismatches, e.g. {bad[:5]}"
+    v = ref.valid
+    np.testing.assert_allclose(bm.max_abs_mo[v], ref.max_abs_mo[v], rtol=RTOL, atol=0)
