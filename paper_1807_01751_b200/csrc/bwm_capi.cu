@@ -254,6 +254,8 @@ struct bwm_plan {
     int occ_raw[3] = {0, 0, 0};        // occupancy API result before the TMEM cap
     bool force_ldg = false;            // BWM_KERNEL=ldg (A/B against the TMA kernel)
     bool const_bound = false;          // b_j == b_0 for every j (LEAN TMA variant applies)
+    bool precise = false;              // long horizon: float64 fitted values, LDG kernels only
+    double* d_xtd = nullptr;           // [N][sp] Z^T in float64 (precise)
     int bpm_tma_lean = 0;              // resident CTAs per SM of the LEAN TMA variant
     // masked-NaN mode (bwm_kernel_masked.cuh)
     bool masked = false;
@@ -291,6 +293,7 @@ static void plan_free_tables(bwm_plan* plan) {
     cudaFree(plan->d_xt);
     cudaFree(plan->d_bound);
     cudaFree(plan->d_rinv);
+    cudaFree(plan->d_xtd);
     cudaFree(plan->d_xx);
     cudaFree(plan->d_gfull);
     cudaFree(plan->d_ring);
@@ -536,12 +539,31 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         }
     for (int j = 0; j < N - n; ++j) bd[j] = (float)tb->bound[j];
     for (size_t i = 0; i < ri.size(); ++i) ri[i] = (float)Rinv[i];
+    // Long monitoring horizons: the fitted value of a far-extrapolated date carries the float32
+    // error of (t - tc)/ts times the trend coefficient, which the MOSUM scale 1/(sigma sqrt n)
+    // can amplify past 1e-4 (fuzz: N/n = 15).  Beyond |(t - tc)/ts| = 8 (N/n ~ 4.5 on a regular
+    // axis) the fitted values are computed in float64 (LDG kernel, float64 Z^T).
+    double s_max = 0.0;
+    for (int t = n; t < N; ++t) s_max = std::max(s_max, std::fabs(tb->design[(size_t)1 * N + t]));
+    const char* prec_env = getenv("BWM_PRECISE");
+    plan->precise = prec_env ? std::strcmp(prec_env, "1") == 0 : s_max > 8.0;
+    std::vector<double> xtd;
+    if (plan->precise) {
+        xtd.assign((size_t)N * sp, 0.0);
+        for (int t = 0; t < N; ++t)
+            for (int i = 0; i < p; ++i) {
+                double z = 0.0;
+                for (int k = 0; k <= i; ++k) z += Rinv[(size_t)k * p + i] * tb->design[(size_t)k * N + t];
+                xtd[(size_t)t * sp + i] = t < n ? Q[(size_t)t * p + i] : z;
+            }
+    }
 
     auto fail = [&](cudaError_t e, const char* what) {
         cudaFree(plan->d_mt);
         cudaFree(plan->d_xt);
         cudaFree(plan->d_bound);
         cudaFree(plan->d_rinv);
+        cudaFree(plan->d_xtd);
         delete plan;
         return set_err((int)e, "%s: %s", what, cudaGetErrorString(e));
     };
@@ -559,6 +581,11 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     if ((e = cudaMalloc(&plan->d_rinv, ri.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
     if ((e = cudaMemcpy(plan->d_rinv, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
+    if (plan->precise) {
+        if ((e = cudaMalloc(&plan->d_xtd, xtd.size() * 8)) != cudaSuccess) return fail(e, "cudaMalloc");
+        if ((e = cudaMemcpy(plan->d_xtd, xtd.data(), xtd.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return fail(e, "cudaMemcpy");
+    }
 
     // LEAN TMA variant: the boundary is one value over the whole monitoring period
     plan->const_bound = true;
@@ -685,6 +712,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     k.mosum = out->mosum;
     k.ld_out = out->ld_out;
     k.zero_sigma = reinterpret_cast<unsigned long long*>(out->zero_sigma_pixel);
+    k.xtd = plan->precise ? plan->d_xtd : nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     int launched = 0;
 
@@ -710,7 +738,8 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     const bool out_al = al(out->valid, 2) && al(out->first_idx, 8) && al(out->max_abs, 8) &&
                         (!out->mo_mean || al(out->mo_mean, 8)) && (!out->beta || al(out->beta, 8)) &&
                         (!out->mosum || al(out->mosum, 8)) && (out->ld_out % 2 == 0 || (!out->beta && !out->mosum));
-    const bool tma_ok = !plan->masked && !plan->force_ldg && plan->smem_tma > 0 && al(y, 16) && (ld_y % 4 == 0) && out_al;
+    const bool tma_ok = !plan->masked && !plan->force_ldg && !plan->precise && plan->smem_tma > 0 && al(y, 16) &&
+                        (ld_y % 4 == 0) && out_al;
     const bool ldg_ok = al(y, 8) && (ld_y % 2 == 0);
     const Kind main_kind = tma_ok ? kTma : kLdgFast;
     const int64_t full = (tma_ok || ldg_ok) ? (n_pixels / bwm::kTile) * bwm::kTile : 0;
@@ -1152,6 +1181,7 @@ int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {
     info->smem_masked = plan->smem_masked;
     info->const_bound = plan->const_bound ? 1 : 0;
     info->ctas_per_sm_tma_lean = plan->bpm_tma_lean;
+    info->precise = plan->precise ? 1 : 0;
     return BWM_OK;
 }
 

@@ -50,6 +50,9 @@ struct KParams {
     const double* gfull;        // [KK] sum of those rows over the whole history
     float* ring_g;              // per-CTA residual rings [grid][h][128] when they live in global memory
     float lambda;               // crit = bound[0]
+    // long monitoring horizons (LDG kernel): fitted values in float64 from this [N][sp] table
+    // (Z^T in double) and the compensated beta_Q, so the trend extrapolation keeps 1e-4
+    const double* xtd;          // nullptr: float32 fitted values (the default)
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -102,6 +105,20 @@ __device__ __forceinline__ float2 dot_row(float2 r, const float* __restrict__ xr
         if (4 * q + 3 < NP) r = fma2s(nb[4 * q + 3], x.w, r);
     }
     return r;
+}
+
+// r = y_c - z^T beta_Q with z from the float64 table and beta_Q = hi + lo in float64 (precise mode)
+template <int NP, int SP>
+__device__ __forceinline__ float2 resid_f64(float2 vc, const double* __restrict__ zrow, const double (&b0)[NP],
+                                            const double (&b1)[NP]) {
+    double r0 = (double)vc.x, r1 = (double)vc.y;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        const double z = __ldg(zrow + i);
+        r0 = fma(-z, b0[i], r0);
+        r1 = fma(-z, b1[i], r1);
+    }
+    return f2((float)r0, (float)r1);
 }
 
 // part_i += vc * m_i

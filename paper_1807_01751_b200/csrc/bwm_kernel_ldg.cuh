@@ -113,6 +113,26 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         float2 part[NP], qpart = f2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < NP; ++i) part[i] = f2(0.f, 0.f);
+        // precise mode (long horizons): beta_Q and ||y - c||^2 also accumulated in float64 — the
+        // float32 block partials' rounding, multiplied by a far-extrapolated z_t, is what limits
+        // the fitted value there
+        const double* const xtd = prm.xtd;
+        double pd0[NP], pd1[NP], qd0 = 0.0, qd1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) pd0[i] = pd1[i] = 0.0;
+        auto acc_f64 = [&](float2 vc, int t) {
+            if (!xtd) return;
+            const double a = (double)vc.x, b = (double)vc.y;
+            const double* z = xtd + (int64_t)t * SP;
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                const double zz = __ldg(z + i);
+                pd0[i] = fma(a, zz, pd0[i]);
+                pd1[i] = fma(b, zz, pd1[i]);
+            }
+            qd0 = fma(a, a, qd0);
+            qd1 = fma(b, b, qd1);
+        };
         for (int t0 = 0; t0 < n; t0 += D) {
             if (t0 + 2 * D <= n) {
 #pragma unroll
@@ -123,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                     const float2 vc = fill(v, negc, last);
                     axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
                     qpart = fma2(vc, vc, qpart);
+                    acc_f64(vc, t0 + k);
                 }
             } else {
 #pragma unroll
@@ -136,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                         const float2 vc = fill(v, negc, last);
                         axpy_row<NP, SP>(part, vc, s_mt + t * SP);
                         qpart = fma2(vc, vc, qpart);
+                        acc_f64(vc, t);
                     } else if (k < N) {
                         buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);      // free slot: pass-2 row k
                     }
@@ -150,9 +172,24 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
             }
         }
         float2 bq[NP], nb[NP];    // beta_Q and -beta_Q
+        double bd0[NP], bd1[NP];  // precise mode: beta_Q in float64
+        double sd0 = 0.0, sd1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < NP; ++i) { bq[i] = add2(hi[i], lo[i]); nb[i] = f2(-bq[i].x, -bq[i].y); }
-        const float2 ss = rss_onepass<NP>(q0, q1, bq);
+        for (int i = 0; i < NP; ++i) {
+            bq[i] = add2(hi[i], lo[i]);
+            nb[i] = f2(-bq[i].x, -bq[i].y);
+            bd0[i] = pd0[i];
+            bd1[i] = pd1[i];
+            sd0 = fma(pd0[i], pd0[i], sd0);
+            sd1 = fma(pd1[i], pd1[i], sd1);
+        }
+        // residual of date t (float32 fitted value, or float64 for long horizons: uniform branch)
+        auto resid = [&](float2 vc, int t) -> float2 {
+            if (xtd) return resid_f64<NP, SP>(vc, xtd + (int64_t)t * SP, bd0, bd1);
+            return dot_row<NP, SP>(vc, s_xt + t * SP, nb);
+        };
+        const float2 ss = xtd ? f2((float)fmax(qd0 - sd0, 0.0), (float)fmax(qd1 - sd1, 0.0))
+                              : rss_onepass<NP>(q0, q1, bq);
 
         // ---- pass 2: fill state through the history; residuals of window 0 --------------
         float2 acc = f2(0.f, 0.f);
@@ -182,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                         pf += ld;
                         const float2 vc = fill(v, negc, last);
                         if (t >= wstart) {
-                            const float2 r = dot_row<NP, SP>(vc, s_xt + t * SP, nb);
+                            const float2 r = resid(vc, t);
                             acc = add2(acc, r);
                             if (RING) {
                                 ring[slot * kThreads] = r;
@@ -213,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
             if (fast || t + D < N) buf[k] = ldp<SAFE>(pf, npx);
             else if (has_next && k < n) buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);
             float2 old = f2(0.f, 0.f);
-            const float2 r = dot_row<NP, SP>(fill(v, negc, last), s_xt + t * SP, nb);
+            const float2 r = resid(fill(v, negc, last), t);
             if (RING) {
                 old = ring[slot * kThreads];
                 ring[slot * kThreads] = r;
@@ -222,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                 if (fast || t > n) {     // r_{t-h}; at t == n, r_{n-h} is outside window 0
                     const float2 lv = (fast || t >= D) ? lbuf[RING ? 0 : k]
                                                        : ldp<SAFE>(pf - (int64_t)D * ld - hld, npx);
-                    old = dot_row<NP, SP>(fill(lv, negc, lag_last), s_xt + (t - h) * SP, nb);
+                    old = resid(fill(lv, negc, lag_last), t - h);
                 }
                 if (fast || t + D < N) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
             }

@@ -95,3 +95,46 @@ def test_random_geometry_masked(i, N, n, h, k, P, nan, irregular):
     assert bad.size == 0, f"{bad.size} mismatches, e.g. {bad[:5]}"
     v = ref.valid
     np.testing.assert_allclose(bm.max_abs_mo[v], ref.max_abs_mo[v], rtol=RTOL, atol=0)
+
+
+@pytest.mark.parametrize("i,N,n,h,k,P,irregular", [(16, 313, 20, 5, 2, 2704, True), (30, 600, 40, 12, 3, 2000, False),
+                                                   (31, 900, 60, 30, 4, 1500, True)])
+def test_long_horizon_precise(i, N, n, h, k, P, irregular):
+    """Monitoring horizons far beyond 4x the history (N/n = 10-16): the plan switches to float64
+    fitted values (plan_info precise) and stays within tolerance where float32 did not (case 16
+    reached 2e-4 on max |MO| before)."""
+    import paper_1807_01751_b200 as pkg
+    from paper_1807_01751_b200.device import DevicePlan
+    from paper_1807_01751_b200.synth import host_stack
+
+    rng = np.random.default_rng(100 + i)
+    t = np.cumsum(rng.uniform(1, 9, N)) + 1.0 if irregular else np.arange(1.0, N + 1.0)
+    freq = 365.25 if irregular else 23.0
+    y = host_stack(P, t, freq, n, 0.2, seed=200 + i)
+    cfg = pkg.MonitorConfig(history=n, bandwidth=h, harmonics=k, freq=freq, crit_value=3.0)
+    assert DevicePlan.get(pkg.TimeAxis(t), freq, k, n, h, 3.0).info()["precise"] == 1
+    ref = bo.monitor(y, t, n, h, k, freq, 3.0, keep_mosum=True)
+    bm = pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+    assert np.array_equal(bm.valid, ref.valid)
+    first_gpu = np.where(bm.first_break > 0, bm.first_break - n, 0)
+    pairs = bo.near_pairs(ref.mosum, bo.boundary(n, N, 3.0))
+    border = bo.borderline_from_pairs(pairs, N - n, P, ref.first_idx, first_gpu)
+    assert not np.any((first_gpu != ref.first_idx) & ~border & ref.valid)
+    np.testing.assert_allclose(bm.max_abs_mo[ref.valid], ref.max_abs_mo[ref.valid], rtol=RTOL, atol=0)
+
+
+def test_precise_mode_on_baseline_geometry(monkeypatch):
+    """BWM_PRECISE=1 forces the float64 fitted values on a C1 geometry: same decisions, within
+    tolerance of the float32 default."""
+    import paper_1807_01751_b200 as pkg
+    from paper_1807_01751_b200.device import DevicePlan
+    from tests.golden_cases import load
+    from tests.test_gpu_parity import check_parity, config_for
+
+    case = load("c1")
+    monkeypatch.setenv("BWM_PRECISE", "1")
+    DevicePlan._cache.clear()
+    bm = pkg.monitor_batch(pkg.SeriesStack(case.y, pkg.TimeAxis(case.t)), config_for(case))
+    assert DevicePlan.get(pkg.TimeAxis(case.t), case.freq, case.k, case.n, case.h, case.crit).info()["precise"] == 1
+    DevicePlan._cache.clear()
+    check_parity(case, bm.first_break, bm.max_abs_mo, bm.valid)
