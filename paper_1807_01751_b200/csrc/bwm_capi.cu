@@ -43,6 +43,8 @@ BWM_DECLARE_PICK_MASKED(16)
 BWM_DECLARE_PICK_MASKED(18)
 
 namespace bwm {
+cudaError_t launch_fixup(const KParams& prm, int p, const int64_t* list, const unsigned int* count, int sms,
+                         cudaStream_t s);
 cudaError_t launch_finalize(const int32_t* first_idx, const float* max_abs, int64_t P, int n, int64_t* first_break,
                             double* mx64, uint8_t* detected, cudaStream_t s);
 }
@@ -255,7 +257,13 @@ struct bwm_plan {
     bool force_ldg = false;            // BWM_KERNEL=ldg (A/B against the TMA kernel)
     bool const_bound = false;          // b_j == b_0 for every j (LEAN TMA variant applies)
     bool precise = false;              // long horizon: float64 fitted values, LDG kernels only
-    double* d_xtd = nullptr;           // [N][sp] Z^T in float64 (precise)
+    double* d_xtd = nullptr;           // [N][sp] Z^T in float64 (precise mode and the fixup)
+    // float64 fixup of ill-conditioned pixels (bwm_fixup.cu): device list + count, grown on use
+    float fix_ratio = 300.f;     // ||y-c||^2 / RSS above which a pixel is recomputed in float64
+    mutable std::mutex fix_mu;
+    mutable int64_t* d_fix_list = nullptr;
+    mutable unsigned int* d_fix_count = nullptr;
+    mutable int64_t fix_cap = 0;
     int bpm_tma_lean = 0;              // resident CTAs per SM of the LEAN TMA variant
     // masked-NaN mode (bwm_kernel_masked.cuh)
     bool masked = false;
@@ -294,6 +302,8 @@ static void plan_free_tables(bwm_plan* plan) {
     cudaFree(plan->d_bound);
     cudaFree(plan->d_rinv);
     cudaFree(plan->d_xtd);
+    cudaFree(plan->d_fix_list);
+    cudaFree(plan->d_fix_count);
     cudaFree(plan->d_xx);
     cudaFree(plan->d_gfull);
     cudaFree(plan->d_ring);
@@ -545,10 +555,12 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     // axis) the fitted values are computed in float64 (LDG kernel, float64 Z^T).
     double s_max = 0.0;
     for (int t = n; t < N; ++t) s_max = std::max(s_max, std::fabs(tb->design[(size_t)1 * N + t]));
+    const char* fix_env = getenv("BWM_FIX_RATIO");                   // 0 disables the fixup
+    if (fix_env) plan->fix_ratio = (float)std::atof(fix_env);
     const char* prec_env = getenv("BWM_PRECISE");
     plan->precise = prec_env ? std::strcmp(prec_env, "1") == 0 : s_max > 8.0;
     std::vector<double> xtd;
-    if (plan->precise) {
+    {
         xtd.assign((size_t)N * sp, 0.0);
         for (int t = 0; t < N; ++t)
             for (int i = 0; i < p; ++i) {
@@ -581,7 +593,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     if ((e = cudaMalloc(&plan->d_rinv, ri.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
     if ((e = cudaMemcpy(plan->d_rinv, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
-    if (plan->precise) {
+    {
         if ((e = cudaMalloc(&plan->d_xtd, xtd.size() * 8)) != cudaSuccess) return fail(e, "cudaMalloc");
         if ((e = cudaMemcpy(plan->d_xtd, xtd.data(), xtd.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
             return fail(e, "cudaMemcpy");
@@ -743,12 +755,35 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     const bool ldg_ok = al(y, 8) && (ld_y % 2 == 0);
     const Kind main_kind = tma_ok ? kTma : kLdgFast;
     const int64_t full = (tma_ok || ldg_ok) ? (n_pixels / bwm::kTile) * bwm::kTile : 0;
+    // float64 fixup list for ill-conditioned pixels (fill mode, float32 kernels)
+    const bool fixup = !plan->masked && !plan->precise && plan->fix_ratio > 0.f && plan->d_xtd;
+    if (fixup) {
+        std::lock_guard<std::mutex> lk(plan->fix_mu);
+        if (plan->fix_cap < n_pixels) {
+            cudaFree(plan->d_fix_list);
+            plan->d_fix_list = nullptr;
+            plan->fix_cap = 0;
+            cudaError_t e = cudaMalloc(&plan->d_fix_list, (size_t)n_pixels * sizeof(int64_t));
+            if (e != cudaSuccess) return set_err((int)e, "fixup list allocation failed: %s", cudaGetErrorString(e));
+            plan->fix_cap = n_pixels;
+            if (!plan->d_fix_count) {
+                e = cudaMalloc(&plan->d_fix_count, sizeof(unsigned int));
+                if (e != cudaSuccess) return set_err((int)e, "fixup count allocation failed: %s", cudaGetErrorString(e));
+            }
+        }
+        cudaError_t e = cudaMemsetAsync(plan->d_fix_count, 0, sizeof(unsigned int), st);
+        if (e != cudaSuccess) return set_err((int)e, "cudaMemsetAsync failed: %s", cudaGetErrorString(e));
+        k.fix_list = plan->d_fix_list;
+        k.fix_count = plan->d_fix_count;
+        k.fix_ratio = plan->fix_ratio;
+    }
     for (int part = 0; part < 2 && !plan->masked; ++part) {
         const Kind kind = part == 0 ? main_kind : kLdgSafe;
         const int64_t p0 = part == 0 ? 0 : full;
         const int64_t cnt = part == 0 ? full : n_pixels - full;
         if (cnt <= 0) continue;
         bwm::KParams kp = k;
+        kp.fix_base = p0;
         kp.y = y + p0;
         kp.n_pixels = cnt;
         kp.pixel_offset = pixel_offset + p0;
@@ -772,6 +807,13 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         fn<<<(unsigned)grid, threads_of(kind), sm, st>>>(kp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
+        ++launched;
+    }
+    if (fixup) {
+        bwm::KParams kf = k;
+        kf.xtd = plan->d_xtd;
+        cudaError_t e = bwm::launch_fixup(kf, d.n_params, plan->d_fix_list, plan->d_fix_count, plan->sms, st);
+        if (e != cudaSuccess) return set_err((int)e, "fixup launch failed: %s", cudaGetErrorString(e));
         ++launched;
     }
     if (out->first_break || out->max_abs_f64 || out->detected) {

@@ -53,7 +53,19 @@ struct KParams {
     // long monitoring horizons (LDG kernel): fitted values in float64 from this [N][sp] table
     // (Z^T in double) and the compensated beta_Q, so the trend extrapolation keeps 1e-4
     const double* xtd;          // nullptr: float32 fitted values (the default)
+    // ill-conditioned pixels (||y-c||^2 > fix_ratio * RSS) are listed for the float64 fixup
+    // (bwm_fixup.cu); list entries are pixel indices of the bwm_monitor call (launch + fix_base)
+    int64_t* fix_list;          // nullptr: no fixup
+    unsigned int* fix_count;
+    float fix_ratio;
+    int64_t fix_base;
 };
+
+// append pixel `px` (launch-relative) to the fixup list when its history fit is ill-conditioned
+__device__ __forceinline__ void fix_flag(const KParams& prm, bool valid, double q, float rss, int64_t px) {
+    if (prm.fix_list && valid && rss > 0.f && q > (double)prm.fix_ratio * (double)rss)
+        prm.fix_list[atomicAdd(prm.fix_count, 1u)] = prm.fix_base + px;
+}
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }

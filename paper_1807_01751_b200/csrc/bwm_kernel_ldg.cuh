@@ -190,6 +190,10 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         };
         const float2 ss = xtd ? f2((float)fmax(qd0 - sd0, 0.0), (float)fmax(qd1 - sd1, 0.0))
                               : rss_onepass<NP>(q0, q1, bq);
+        if (!xtd) {
+            fix_flag(prm, valid0, q0, ss.x, px0);
+            fix_flag(prm, valid1, q1, ss.y, px0 + 1);
+        }
 
         // ---- pass 2: fill state through the history; residuals of window 0 --------------
         float2 acc = f2(0.f, 0.f);

@@ -418,6 +418,8 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         // sigma ~1e-17 there (MO ~1e15): scale 0 reproduces its decisions (any non-zero window
         // crosses).
         const float2 ss = rss_onepass<NP>(q0, q1, bq);
+        fix_flag(prm, valid0, q0, ss.x, px0);
+        fix_flag(prm, valid1, q1, ss.y, px0 + 1);
         const bool z0 = valid0 && ss.x == 0.f && c.x == 0.f, z1 = valid1 && ss.y == 0.f && c.y == 0.f;
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
         const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);

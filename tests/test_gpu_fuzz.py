@@ -138,3 +138,39 @@ def test_precise_mode_on_baseline_geometry(monkeypatch):
     assert DevicePlan.get(pkg.TimeAxis(case.t), case.freq, case.k, case.n, case.h, case.crit).info()["precise"] == 1
     DevicePlan._cache.clear()
     check_parity(case, bm.first_break, bm.max_abs_mo, bm.valid)
+
+
+@pytest.mark.parametrize("i,sigma", [(0, 0.005), (1, 0.002), (2, 0.001), (3, 0.003)])
+def test_low_noise(i, sigma):
+    """Low-noise stacks (||y - c||^2 / RSS up to ~1e4, the cancellation the one-pass RSS must
+    survive) with leading gaps and long NaN runs; C1-C3 and C4/C5-like geometries."""
+    import paper_1807_01751_b200 as pkg
+
+    rng = np.random.default_rng(500 + i)
+    N, n, h, k, freq = [(228, 114, 28, 3, 23.0), (400, 200, 50, 3, 365.25), (1000, 500, 250, 6, 365.25),
+                        (160, 80, 8, 8, 23.0)][i]
+    t = np.arange(1.0, N + 1.0) if freq == 23.0 else np.cumsum(rng.uniform(1, 9, N)) + 1.0
+    P = 1500
+    phi = rng.uniform(0, 2 * np.pi, P)
+    y = 0.5 + 0.2 * np.sin(2 * np.pi * t[:, None] / freq + phi[None, :]) + rng.normal(0, sigma, (N, P))
+    brk = rng.random(P) < 0.5
+    start = rng.integers(n, N, P)
+    y += ((np.arange(N)[:, None] >= start[None, :]) & brk[None, :]) * rng.uniform(-0.05, -0.01, P)[None, :]
+    y = y.astype(np.float32)
+    y[rng.random((N, P)) < 0.2] = np.nan
+    y[: rng.integers(1, 30), : P // 10] = np.nan            # leading gaps
+    for c in rng.integers(0, P, 50):                          # long NaN runs
+        a = int(rng.integers(0, N - 20))
+        y[a:a + int(rng.integers(5, 20)), c] = np.nan
+    cfg = pkg.MonitorConfig(history=n, bandwidth=h, harmonics=k, freq=freq, crit_value=3.0)
+    ref = bo.monitor(y, t, n, h, k, freq, 3.0, keep_mosum=True)
+    bm = pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+    assert np.array_equal(bm.valid, ref.valid)
+    first_gpu = np.where(bm.first_break > 0, bm.first_break - n, 0)
+    pairs = bo.near_pairs(ref.mosum, bo.boundary(n, N, 3.0))
+    border = bo.borderline_from_pairs(pairs, N - n, P, ref.first_idx, first_gpu)
+    filled, _ = bo.fill_block(y)
+    degen = (filled[:n] == filled[0]).all(axis=0)
+    assert not np.any((first_gpu != ref.first_idx) & ~border & ~degen & ref.valid)
+    ok = ref.valid & ~degen
+    np.testing.assert_allclose(bm.max_abs_mo[ok], ref.max_abs_mo[ok], rtol=RTOL, atol=0)
