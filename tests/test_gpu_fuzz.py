@@ -174,3 +174,28 @@ def test_low_noise(i, sigma):
     assert not np.any((first_gpu != ref.first_idx) & ~border & ~degen & ref.valid)
     ok = ref.valid & ~degen
     np.testing.assert_allclose(bm.max_abs_mo[ok], ref.max_abs_mo[ok], rtol=RTOL, atol=0)
+
+
+@pytest.mark.parametrize("i,sigma", [(0, 0.003), (1, 0.001)])
+def test_low_noise_masked(i, sigma):
+    """Masked mode on near-noiseless series with per-pixel gaps (per-pixel float32 Cholesky
+    plus one refinement step, against the per-pixel float64 oracle)."""
+    import paper_1807_01751_b200 as pkg
+
+    rng = np.random.default_rng(700 + i)
+    N, n, h, k, freq = [(228, 114, 28, 3, 23.0), (400, 200, 50, 3, 365.25)][i]
+    t = np.arange(1.0, N + 1.0) if freq == 23.0 else np.cumsum(rng.uniform(8, 24, N)) + 1.0
+    P = 600
+    phi = rng.uniform(0, 2 * np.pi, P)
+    y = 0.5 + 0.2 * np.sin(2 * np.pi * t[:, None] / freq + phi[None, :]) + rng.normal(0, sigma, (N, P))
+    brk = rng.random(P) < 0.5
+    start = rng.integers(n, N, P)
+    y += ((np.arange(N)[:, None] >= start[None, :]) & brk[None, :]) * rng.uniform(-0.05, -0.01, P)[None, :]
+    y = y.astype(np.float32)
+    y[rng.random((N, P)) < 0.25] = np.nan
+    cfg = pkg.MonitorConfig(history=n, bandwidth=h, harmonics=k, freq=freq, crit_value=3.0, nan_mode="mask")
+    ref = bo.monitor_masked(y, t, n, h, k, freq, 3.0)
+    bm = pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+    assert np.array_equal(bm.valid, ref.valid)
+    assert not np.any((bm.first_break != ref.first_break) & ~ref.near & ref.valid)
+    np.testing.assert_allclose(bm.max_abs_mo[ref.valid], ref.max_abs_mo[ref.valid], rtol=RTOL, atol=0)
