@@ -45,6 +45,7 @@ BWM_DECLARE_PICK_MASKED(18)
 namespace bwm {
 cudaError_t launch_fixup(const KParams& prm, int p, const int64_t* list, const unsigned int* count, int sms,
                          cudaStream_t s);
+cudaError_t launch_masked_f64(const KParams& prm, int p, double lambda, int sms, cudaStream_t s);
 cudaError_t launch_finalize(const int32_t* first_idx, const float* max_abs, int64_t P, int n, int64_t* first_break,
                             double* mx64, uint8_t* detected, cudaStream_t s);
 }
@@ -259,6 +260,7 @@ struct bwm_plan {
     bool precise = false;              // long horizon: float64 fitted values, LDG kernels only
     double* d_xtd = nullptr;           // [N][sp] Z^T in float64 (precise mode and the fixup)
     // float64 fixup of ill-conditioned pixels (bwm_fixup.cu): device list + count, grown on use
+    double lambda_d = 0.0;            // masked float64 kernel
     float fix_ratio = 300.f;     // ||y-c||^2 / RSS above which a pixel is recomputed in float64
     mutable std::mutex fix_mu;
     mutable int64_t* d_fix_list = nullptr;
@@ -398,6 +400,26 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
     if ((e = cudaMemcpy(plan->d_gfull, gf.data(), gf.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
     plan->lambda = (float)tb->bound[0];    // bound_0 = crit * sqrt(log_plus((n+1)/n)) = crit
+    plan->lambda_d = tb->bound[0];
+    {
+        // long monitoring horizons: every pixel through the float64 masked kernel (bwm_fixup.cu)
+        double s_max = 0.0;
+        for (int t = n; t < N; ++t) s_max = std::max(s_max, std::fabs(tb->design[(size_t)1 * N + t]));
+        const char* prec_env = getenv("BWM_PRECISE");
+        plan->precise = prec_env ? std::strcmp(prec_env, "1") == 0 : s_max > 8.0;
+        if (plan->precise) {
+            std::vector<double> xd((size_t)N * sp, 0.0);
+            for (int t = 0; t < N; ++t)
+                for (int i = 0; i < p; ++i) xd[(size_t)t * sp + i] = tb->design[(size_t)i * N + t];
+            cudaError_t e2 = cudaMalloc(&plan->d_xtd, xd.size() * 8);
+            if (e2 == cudaSuccess) e2 = cudaMemcpy(plan->d_xtd, xd.data(), xd.size() * 8, cudaMemcpyHostToDevice);
+            if (e2 != cudaSuccess) {
+                plan_free_tables(plan);
+                delete plan;
+                return set_err((int)e2, "masked float64 table: %s", cudaGetErrorString(e2));
+            }
+        }
+    }
     KernelFn fn = pick_masked(p, plan->mbig, false);
     for (int keep = 0; keep < 2; ++keep)
         if ((e = cudaFuncSetAttribute((const void*)pick_masked(p, plan->mbig, keep), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -728,7 +750,13 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     cudaStream_t st = (cudaStream_t)stream;
     int launched = 0;
 
-    if (plan->masked) {
+    if (plan->masked && plan->precise) {
+        bwm::KParams kf = k;
+        kf.xtd = plan->d_xtd;
+        cudaError_t e = bwm::launch_masked_f64(kf, d.n_params, plan->lambda_d, plan->sms, st);
+        if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
+        ++launched;
+    } else if (plan->masked) {
         // one launch, any alignment (scalar predicated loads and stores)
         k.xx = plan->d_xx;
         k.gfull = plan->d_gfull;

@@ -199,3 +199,26 @@ def test_low_noise_masked(i, sigma):
     assert np.array_equal(bm.valid, ref.valid)
     assert not np.any((bm.first_break != ref.first_break) & ~ref.near & ref.valid)
     np.testing.assert_allclose(bm.max_abs_mo[ref.valid], ref.max_abs_mo[ref.valid], rtol=RTOL, atol=0)
+
+
+@pytest.mark.parametrize("i,N,n,h,k", [(0, 600, 150, 30, 3), (1, 320, 80, 12, 2), (2, 400, 100, 25, 4),
+                                       (3, 600, 60, 15, 3), (4, 313, 30, 6, 2)])
+def test_long_horizon_masked(i, N, n, h, k):
+    """Masked mode with monitoring horizons of 4x the history (float32 kernel) and of 10x
+    (the plan switches to the per-pixel float64 masked kernel)."""
+    import paper_1807_01751_b200 as pkg
+    from paper_1807_01751_b200.synth import host_stack
+
+    rng = np.random.default_rng(800 + i)
+    t = np.cumsum(rng.uniform(1, 9, N)) + 1.0
+    y = host_stack(600, t, 365.25, n, 0.2, seed=900 + i)
+    cfg = pkg.MonitorConfig(history=n, bandwidth=h, harmonics=k, freq=365.25, crit_value=3.0, nan_mode="mask")
+    from paper_1807_01751_b200.device import DevicePlan
+
+    precise = DevicePlan.get(pkg.TimeAxis(t), 365.25, k, n, h, 3.0, nan_mode="mask").info()["precise"]
+    assert precise == (1 if N >= 5 * n else 0)
+    ref = bo.monitor_masked(y, t, n, h, k, 365.25, 3.0)
+    bm = pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), cfg)
+    assert np.array_equal(bm.valid, ref.valid)
+    assert not np.any((bm.first_break != ref.first_break) & ~ref.near & ref.valid)
+    np.testing.assert_allclose(bm.max_abs_mo[ref.valid], ref.max_abs_mo[ref.valid], rtol=RTOL, atol=0)
