@@ -787,13 +787,16 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     const bool fixup = !plan->masked && !plan->precise && plan->fix_ratio > 0.f && plan->d_xtd;
     if (fixup) {
         std::lock_guard<std::mutex> lk(plan->fix_mu);
-        if (plan->fix_cap < n_pixels) {
+        // capacity: every pixel of small calls, 4M entries (32 MB) at most — flagged pixels are
+        // rare on real data, and a near-capacity stack must not run out of HBM for the list
+        const int64_t want = std::min<int64_t>(n_pixels, 4ll << 20);
+        if (plan->fix_cap < want) {
             cudaFree(plan->d_fix_list);
             plan->d_fix_list = nullptr;
             plan->fix_cap = 0;
-            cudaError_t e = cudaMalloc(&plan->d_fix_list, (size_t)n_pixels * sizeof(int64_t));
+            cudaError_t e = cudaMalloc(&plan->d_fix_list, (size_t)want * sizeof(int64_t));
             if (e != cudaSuccess) return set_err((int)e, "fixup list allocation failed: %s", cudaGetErrorString(e));
-            plan->fix_cap = n_pixels;
+            plan->fix_cap = want;
             if (!plan->d_fix_count) {
                 e = cudaMalloc(&plan->d_fix_count, sizeof(unsigned int));
                 if (e != cudaSuccess) return set_err((int)e, "fixup count allocation failed: %s", cudaGetErrorString(e));
@@ -803,6 +806,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         if (e != cudaSuccess) return set_err((int)e, "cudaMemsetAsync failed: %s", cudaGetErrorString(e));
         k.fix_list = plan->d_fix_list;
         k.fix_count = plan->d_fix_count;
+        k.fix_cap = (unsigned int)plan->fix_cap;
         k.fix_ratio = plan->fix_ratio;
     }
     for (int part = 0; part < 2 && !plan->masked; ++part) {

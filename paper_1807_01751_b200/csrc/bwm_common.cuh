@@ -18,7 +18,10 @@ namespace bwm {
 constexpr int kThreads = 128;
 constexpr int kTile = 2 * kThreads;   // pixels per CTA tile
 constexpr int kDepth = 16;            // LDG kernel: prefetch depth == compensation block (dates)
-constexpr int kComp = 32;             // dates per 2Sum-compensated block partial (emulated 1e-5)
+#ifndef BWM_COMP
+#define BWM_COMP 32
+#endif
+constexpr int kComp = BWM_COMP;       // dates per 2Sum-compensated block partial (emulated 1e-5 at 32)
 
 struct KParams {
     CUtensorMap tmap;           // TMA kernel: 2-D map of y (pixels x dates), box 64 px x 8 dates
@@ -57,14 +60,17 @@ struct KParams {
     // (bwm_fixup.cu); list entries are pixel indices of the bwm_monitor call (launch + fix_base)
     int64_t* fix_list;          // nullptr: no fixup
     unsigned int* fix_count;
+    unsigned int fix_cap;       // list capacity; pixels past it keep their float32 result
     float fix_ratio;
     int64_t fix_base;
 };
 
 // append pixel `px` (launch-relative) to the fixup list when its history fit is ill-conditioned
 __device__ __forceinline__ void fix_flag(const KParams& prm, bool valid, double q, float rss, int64_t px) {
-    if (prm.fix_list && valid && rss > 0.f && q > (double)prm.fix_ratio * (double)rss)
-        prm.fix_list[atomicAdd(prm.fix_count, 1u)] = prm.fix_base + px;
+    if (prm.fix_list && valid && rss > 0.f && q > (double)prm.fix_ratio * (double)rss) {
+        const unsigned int i = atomicAdd(prm.fix_count, 1u);
+        if (i < prm.fix_cap) prm.fix_list[i] = prm.fix_base + px;
+    }
 }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }

@@ -23,7 +23,7 @@ constexpr int kFixMaxP = 18;
 
 __global__ void __launch_bounds__(128) fixup_kernel(const KParams prm, int p, const int64_t* __restrict__ list,
                                                     const unsigned int* __restrict__ count) {
-    const unsigned int cnt = *count;
+    const unsigned int cnt = min(*count, prm.fix_cap);
     const int N = prm.N, n = prm.n, h = prm.h, sp = prm.sp;
     const double* __restrict__ Z = prm.xtd;      // [N][sp] float64 Z^T (rows < n: Q^T)
     const double sqrt_n = sqrt((double)n);
