@@ -140,8 +140,11 @@ __device__ __forceinline__ void chol_col(float (&L)[NP * (NP + 1) / 2], float (&
 // idle lanes of a tail tile read this NaN (stride 0): every date missing, no per-row test
 static __device__ const unsigned int kNanRow[1] = {0x7fc00000u};
 
+#ifndef BWM_MASK_MINB
+#define BWM_MASK_MINB 4
+#endif
 template <int NP, bool BIG, bool KEEP>
-__global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? 4 : 2)
+__global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
     monitor_kernel_masked(const __grid_constant__ KParams prm) {
     constexpr int SP = Coefs<NP>::SP;
     constexpr int KK = Gram<NP>::KK, NN = Gram<NP>::NN, SB = Gram<NP>::SB;
