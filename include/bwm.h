@@ -120,7 +120,11 @@ void bwm_plan_destroy(bwm_plan* plan);
  *   y        : device float32 [N][ld_y], pixel p of this shard at column p
  *   n_pixels : pixels in this shard (P)
  *   pixel_offset : global index of this shard's pixel 0 (for zero_sigma_pixel)
- * No allocation, no synchronisation.  Re-entrant across streams and devices.
+ * No synchronisation.  Allocation only on the first call of a plan (and when a larger call
+ * grows it): the device list of the float64 fixup, at most 4M entries (32 MB) — valid pixels
+ * whose ||y - c||^2 / RSS exceeds 300 (BWM_FIX_RATIO) are recomputed in float64 by a second
+ * launch; plans whose monitoring horizon extrapolates the trend past |(t - tc)/ts| = 8 run
+ * float64 kernels throughout (BWM_PRECISE).  Re-entrant across streams and devices.
  */
 int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pixels,
                 int64_t pixel_offset, const bwm_outputs* out, void* stream);
@@ -132,7 +136,9 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
  * column chunks with the H2D of chunk i+1 overlapping the kernel of chunk i and the D2H
  * of chunk i-1 on separate streams.  y_host may be pageable or pinned (pinned is faster).
  * Blocks until done.  Outputs are host pointers with the same layout as bwm_outputs;
- * first_idx / max_abs may be NULL here when first_break / max_abs_f64 are given.
+ * first_idx / max_abs may be NULL here when first_break / max_abs_f64 are given.  Pageable
+ * (unregistered) stacks are staged through pinned slots by memcpy threads; pageable result
+ * maps receive their D2H through a plan-owned pinned landing zone.
  */
 int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t n_pixels,
                      int64_t pixel_offset, const bwm_outputs* out_host);
