@@ -157,6 +157,15 @@ int bwm_monitor_file(bwm_plan* plan, const char* path, int64_t payload_offset, i
                      int io_threads, const bwm_outputs* out_host);
 
 /*
+ * One rank's share of a BTS1 file: pixels [first_pixel, first_pixel + n_pixels) of a payload
+ * with file_pixels columns (each row block is read as n_pixels-wide pieces).  Outputs are for
+ * those pixels only (index 0 = first_pixel); zero_sigma_pixel reports file pixel indices.
+ * bwm_monitor_file is the whole-file case.
+ */
+int bwm_monitor_file_range(bwm_plan* plan, const char* path, int64_t payload_offset, int64_t file_pixels,
+                           int64_t first_pixel, int64_t n_pixels, int io_threads, const bwm_outputs* out_host);
+
+/*
  * Parallel read of a time-major float32 payload [n_obs][n_pixels] at byte `offset` of a file
  * into dst (any host memory; pinned makes the later H2D faster).  The read half of
  * dataio.read_stack (dataio.py:110-114).  threads < 1: all hardware threads.

@@ -86,6 +86,8 @@ SIGNATURES = [
      [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(Outputs)]),
     ("bwm_monitor_file", C.c_int,
      [C.c_void_p, C.c_char_p, C.c_int64, C.c_int64, C.c_int, C.POINTER(Outputs)]),
+    ("bwm_monitor_file_range", C.c_int,
+     [C.c_void_p, C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.POINTER(Outputs)]),
     ("bwm_read_payload", C.c_int, [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int]),
     ("bwm_write_break_map", C.c_int64,
      [C.c_char_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),

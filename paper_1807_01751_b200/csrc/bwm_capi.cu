@@ -913,7 +913,8 @@ static int pipe_ensure(bwm_plan* plan, int64_t chunk, int nbuf, const PipeNeeds&
 // and bwm_monitor_file (source: a time-major payload file; rectangles are read into pinned
 // slots by a thread pool while earlier rectangles are copied to HBM).
 static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, const bwm::PayloadFile* file,
-                            int io_threads, int64_t n_pixels, int64_t pixel_offset, const bwm_outputs* out) {
+                            int io_threads, int64_t n_pixels, int64_t pixel_offset, const bwm_outputs* out,
+                            int64_t col_base = 0) {
     if (!plan) return set_err(BWM_E_NULL, "plan is NULL");
     if (!(y_host || file) || !out || !out->valid || !out->zero_sigma_pixel || !(out->first_idx || out->first_break) ||
         !(out->max_abs || out->max_abs_f64))
@@ -991,7 +992,9 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
         const char* slot_env = std::getenv("BWM_IO_SLOT_BYTES");     // tests: small slots split rows
         const int64_t slot_bytes = slot_env ? std::max<int64_t>(256, std::atoll(slot_env)) : (32ll << 20);
         for (int64_t c = 0; c < n_chunks; ++c) {
-            bwm::plan_rects(N, c * chunk, std::min(n_pixels, (c + 1) * chunk), c, slot_bytes, &rects);
+            // file columns: this call's pixels start at column col_base of the payload
+            bwm::plan_rects(N, col_base + c * chunk, col_base + std::min(n_pixels, (c + 1) * chunk), c, slot_bytes,
+                            &rects);
             rect_begin.push_back((int64_t)rects.size());
         }
         const int threads = std::max(1, io_threads);
@@ -1063,7 +1066,7 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
                 if (!src) return set_err(BWM_E_IO, "%s", reader.error().c_str());
                 cudaStream_t cs = nbuf == 1 ? hp.s_h2d[g & 1] : sh;
                 const int64_t rw = r.c1 - r.c0;
-                BWM_CUDA(cudaMemcpy2DAsync(hp.d_y[b] + r.r0 * w + (r.c0 - p0), (size_t)w * 4, src, (size_t)rw * 4,
+                BWM_CUDA(cudaMemcpy2DAsync(hp.d_y[b] + r.r0 * w + (r.c0 - col_base - p0), (size_t)w * 4, src, (size_t)rw * 4,
                                            (size_t)rw * 4, (size_t)(r.r1 - r.r0), cudaMemcpyHostToDevice, cs));
                 BWM_CUDA(cudaEventRecord(slot_ev[(size_t)(g % K)], cs));
                 pending.push_back(g);
@@ -1225,16 +1228,24 @@ int bwm_monitor_host(bwm_plan* plan, const float* y_host, int64_t ld_y, int64_t 
     return monitor_pipeline(plan, y_host, ld_y, nullptr, 0, n_pixels, pixel_offset, out_host);
 }
 
-int bwm_monitor_file(bwm_plan* plan, const char* path, int64_t payload_offset, int64_t n_pixels,
-                     int io_threads, const bwm_outputs* out_host) {
+int bwm_monitor_file_range(bwm_plan* plan, const char* path, int64_t payload_offset, int64_t file_pixels,
+                           int64_t first_pixel, int64_t n_pixels, int io_threads, const bwm_outputs* out_host) {
     if (!plan) return set_err(BWM_E_NULL, "plan is NULL");
     if (!path) return set_err(BWM_E_NULL, "path is NULL");
     if (n_pixels < 1) return set_err(BWM_E_DIMS, "stack needs at least one pixel");
+    if (first_pixel < 0 || first_pixel + n_pixels > file_pixels)
+        return set_err(BWM_E_DIMS, "pixel range [%lld, %lld) outside the file's %lld pixels", (long long)first_pixel,
+                       (long long)(first_pixel + n_pixels), (long long)file_pixels);
     bwm::PayloadFile f;
     std::string err;
-    if (int rc = f.open(path, payload_offset, plan->dims.n_obs, n_pixels, &err)) return set_err(rc, "%s", err.c_str());
+    if (int rc = f.open(path, payload_offset, plan->dims.n_obs, file_pixels, &err)) return set_err(rc, "%s", err.c_str());
     if (io_threads < 1) io_threads = (int)std::min(32u, std::max(1u, std::thread::hardware_concurrency()));
-    return monitor_pipeline(plan, nullptr, n_pixels, &f, io_threads, n_pixels, 0, out_host);
+    return monitor_pipeline(plan, nullptr, n_pixels, &f, io_threads, n_pixels, first_pixel, out_host, first_pixel);
+}
+
+int bwm_monitor_file(bwm_plan* plan, const char* path, int64_t payload_offset, int64_t n_pixels,
+                     int io_threads, const bwm_outputs* out_host) {
+    return bwm_monitor_file_range(plan, path, payload_offset, n_pixels, 0, n_pixels, io_threads, out_host);
 }
 
 int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {

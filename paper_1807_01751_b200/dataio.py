@@ -176,19 +176,25 @@ class _FileStack:
     data: object = None
 
 
-def _file_run(path, config, threads, keep_mosum, return_beta, return_mean, device):
+def _file_run(path, config, threads, keep_mosum, return_beta, return_mean, device, pixels=None):
     with open(path, "rb") as handle:
         hdr = read_header(handle)
-    stack = _FileStack(hdr.n_obs, hdr.n_pixels, hdr.time_axis)
+    start, stop = (0, hdr.n_pixels) if pixels is None else (int(pixels[0]), int(pixels[1]))
+    if not 0 <= start < stop <= hdr.n_pixels:
+        raise ValueError(f"pixel range {pixels} outside the file's {hdr.n_pixels} pixels")
+    stack = _FileStack(hdr.n_obs, stop - start, hdr.time_axis)
     return _run(stack, config, threads, DEFAULT_BLOCK_SIZE, keep_mosum, return_beta, return_mean, device,
-                source=(path, hdr.payload_offset))
+                source=(path, hdr.payload_offset, start, hdr.n_pixels))
 
 
 def monitor_file(path, config: MonitorConfig, threads: Optional[int] = None, keep_mosum: bool = False, *,
-                 return_beta: bool = False, return_mean: bool = False, device=None) -> BreakMap:
+                 return_beta: bool = False, return_mean: bool = False, device=None, pixels=None) -> BreakMap:
     """monitor_batch(read_stack(path), config) without the intermediate host copy: the
-    payload streams file -> pinned slots -> HBM with the reads overlapped (bwm_monitor_file)."""
-    return _file_run(path, config, threads, keep_mosum, return_beta, return_mean, device)[0]
+    payload streams file -> pinned slots -> HBM with the reads overlapped (bwm_monitor_file).
+
+    pixels=(start, stop) monitors one pixel band of the file — one rank's shard on a multi-GPU
+    box (sharding.shard_bounds); the BreakMap then covers those pixels only."""
+    return _file_run(path, config, threads, keep_mosum, return_beta, return_mean, device, pixels)[0]
 
 
 def profile_file(path, config: MonitorConfig, threads: Optional[int] = None, *,

@@ -224,15 +224,18 @@ class DevicePlan:
         return self._host_call(call, "bwm_monitor_host", P, keep_mosum, beta, mean, ref_dtypes)
 
     def run_file(self, path, payload_offset: int, n_pixels: int, *, keep_mosum: bool = False, beta: bool = False,
-                 mean: bool = False, io_threads: int = 0, ref_dtypes: bool = True) -> DeviceResult:
+                 mean: bool = False, io_threads: int = 0, ref_dtypes: bool = True, first_pixel: int = 0,
+                 file_pixels: Optional[int] = None) -> DeviceResult:
         """Monitor the time-major payload of a BTS1 file (dataio.py:1-13) straight from disk:
         libbwm reads row blocks into pinned slots on io_threads threads while earlier blocks
-        are copied to HBM (bwm_monitor_file)."""
+        are copied to HBM (bwm_monitor_file_range).  first_pixel / file_pixels select one
+        rank's pixel band of the file."""
         P = int(n_pixels)
+        total = int(file_pixels) if file_pixels is not None else P
         raw = os.fsencode(path)
-        call = lambda o: self._lib.bwm_monitor_file(self._handle, raw, int(payload_offset), P,  # noqa: E731
-                                                    int(io_threads), o)
-        return self._host_call(call, "bwm_monitor_file", P, keep_mosum, beta, mean, ref_dtypes)
+        call = lambda o: self._lib.bwm_monitor_file_range(self._handle, raw, int(payload_offset), total,  # noqa: E731
+                                                          int(first_pixel), P, int(io_threads), o)
+        return self._host_call(call, "bwm_monitor_file_range", P, keep_mosum, beta, mean, ref_dtypes)
 
     def _host_call(self, call, what, P, keep_mosum, beta, mean, ref_dtypes) -> DeviceResult:
         # Plain numpy results: libbwm lands the maps in its own pinned zone and copies them out

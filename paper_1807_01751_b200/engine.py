@@ -286,8 +286,9 @@ def _run(stack, config, threads, block_size, keep_mosum, return_beta, return_mea
             res = plan.run_host(stack.data, keep_mosum=keep_mosum, beta=return_beta, mean=return_mean,
                                 ref_dtypes=True)
         else:
+            first, total = (source[2], source[3]) if len(source) > 2 else (0, stack.n_pixels)
             res = plan.run_file(source[0], source[1], stack.n_pixels, keep_mosum=keep_mosum, beta=return_beta,
-                                mean=return_mean, ref_dtypes=True)
+                                mean=return_mean, ref_dtypes=True, first_pixel=first, file_pixels=total)
         t_kernel = res.kernel_ms * 1e-3
         t_ingest = max(0.0, (res.total_ms - res.kernel_ms) * 1e-3)
         t_d2h = 0.0

@@ -106,3 +106,23 @@ def test_pageable_host_stack(monkeypatch, env):
     _same(got, ref)
     dev = pkg.monitor_batch(pkg.SeriesStack(torch.as_tensor(y, device="cuda"), pkg.TimeAxis(case.t)), cfg)
     _same(dev, pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(case.t)), cfg))
+
+
+def test_file_pixel_ranges_equal_whole(tmp_path):
+    """Each rank's band of one file (monitor_file(pixels=...), bwm_monitor_file_range) gives
+    exactly the corresponding slice of the whole-file maps."""
+    pkg = _pkg()
+    from paper_1807_01751_b200.sharding import shard_bounds
+
+    case = load("c1")
+    path = tmp_path / "s.bts"
+    pkg.write_stack(pkg.SeriesStack(case.y[:, :9001], pkg.TimeAxis(case.t)), path)
+    cfg = config_for(case)
+    whole = pkg.monitor_file(path, cfg, keep_mosum=True)
+    for a, b in shard_bounds(9001, 3, align=4):
+        part = pkg.monitor_file(path, cfg, keep_mosum=True, pixels=(a, b))
+        for f in ("detected", "first_break", "max_abs_mo", "valid"):
+            assert np.array_equal(getattr(part, f), getattr(whole, f)[a:b]), f
+        assert np.array_equal(part.mosum, whole.mosum[:, a:b])
+    with pytest.raises(ValueError):
+        pkg.monitor_file(path, cfg, pixels=(5, 9002))
