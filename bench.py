@@ -49,7 +49,7 @@ def parse():
                          "16384^2 scene split into one pixel band per rank (strong scaling, N >= 2)")
     ap.add_argument("--nan-mode", default="fill", choices=["fill", "mask"],
                     help="fill: the reference's gap fill (headline); mask: per-pixel masked fits (extension)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-file", action="store_true",
                     help="also time monitor_file on a BTS1 copy of the stack (page cache: /dev/shm or /tmp)")
