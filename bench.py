@@ -55,7 +55,10 @@ def parse():
                     help="also time monitor_file on a BTS1 copy of the stack (page cache: /dev/shm or /tmp)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 20, help="pixels in the CPU baseline sample")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps < 1 or args.warmup < 0 or args.e2e_steps < 1:
+        ap.error("--steps and --e2e-steps must be >= 1, --warmup >= 0")
+    return args
 
 
 def peaks():
@@ -86,7 +89,13 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.out = None
+        self.lines: list[str] = []
+        self.reader = None
+        self.error = "nvidia-smi unavailable"
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line)
 
     def __enter__(self):
         try:
@@ -95,7 +104,16 @@ class ClockSampler:
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (FileNotFoundError, OSError):
             self.proc = None
-        time.sleep(0.15)
+            return self
+        import threading
+
+        self.reader = threading.Thread(target=self._read, daemon=True)
+        self.reader.start()
+        t0 = time.monotonic()                  # nvidia-smi takes a few 100 ms to start: wait for
+        while not self.lines and self.proc.poll() is None and time.monotonic() - t0 < 5.0:
+            time.sleep(0.01)                   # its first sample so short timed regions are covered
+        if not self.lines:
+            self.error = "nvidia-smi produced no samples"
         return self
 
     def __exit__(self, *exc):
@@ -104,15 +122,16 @@ class ClockSampler:
         time.sleep(0.1)
         self.proc.terminate()
         try:
-            self.out, _ = self.proc.communicate(timeout=5)
+            self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-            self.out, _ = self.proc.communicate()
+            self.proc.wait()
+        self.reader.join(timeout=5)
 
     def summary(self):
-        if not self.out:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        rows = [[c.strip() for c in line.split(",")] for line in self.out.strip().splitlines() if line.strip()]
+        if not self.lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.error], "samples": 0}
+        rows = [[c.strip() for c in line.split(",")] for line in self.lines if line.strip()]
         sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
         smax = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -319,7 +338,7 @@ def run_ours(args):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = _lib.launch_count()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev.index if dev.index is not None else local) as clocks:
         barrier(world)
         torch.cuda.synchronize()
         torch.cuda.nvtx.range_push("bench_timed")
