@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BWM_ABI_VERSION 5
+#define BWM_ABI_VERSION 6
 
 /* error codes (negative); positive returns are cudaError_t values */
 #define BWM_OK 0
@@ -106,6 +106,10 @@ typedef struct bwm_outputs {
     int64_t* first_break;    /* [P]  n + first_idx, 0 = no break (1-based observation number)     */
     double* max_abs_f64;     /* [P]  max_abs widened to float64                                    */
     uint8_t* detected;       /* [P]  first_break > 0                                               */
+    /* Optional: the Monte Carlo statistic of critical_value (reference mosum.py:166-227),
+       sup_j |MO_j| / bound_j per pixel (with a unit-lambda plan: sup_j |MO_j| / sqrt(log_plus(
+       (n+1+j)/n))), so lambda calibration needs no MOSUM matrix.  Fill mode only.  NULL to skip. */
+    float* sup_stat;         /* [P] */
 } bwm_outputs;
 
 typedef struct bwm_plan bwm_plan;
@@ -124,7 +128,11 @@ void bwm_plan_destroy(bwm_plan* plan);
  * grows it): the device list of the float64 fixup, at most 4M entries (32 MB) — valid pixels
  * whose ||y - c||^2 / RSS exceeds 300 (BWM_FIX_RATIO) are recomputed in float64 by a second
  * launch; plans whose monitoring horizon extrapolates the trend past |(t - tc)/ts| = 8 run
- * float64 kernels throughout (BWM_PRECISE).  Re-entrant across streams and devices.
+ * float64 kernels throughout (BWM_PRECISE).  Re-entrant across streams, host threads and
+ * devices: calls that use the plan's device scratch (the fixup list; the masked-mode rings of
+ * large geometries) are ordered on the device through a plan-owned event, the rest overlap.
+ * zero_sigma_pixel accumulates (atomicMin) across calls until the caller re-initialises it
+ * (bwm_zero_sigma_init).
  */
 int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pixels,
                 int64_t pixel_offset, const bwm_outputs* out, void* stream);
@@ -209,6 +217,10 @@ typedef struct bwm_plan_info_t {
 } bwm_plan_info_t;
 
 int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info);
+
+/* Stream-ordered reset of a device zero_sigma_pixel slot to INT64_MAX (two cudaMemsetAsync,
+   no kernel, no allocation): lets a caller reuse one slot across bwm_monitor calls. */
+int bwm_zero_sigma_init(int64_t* zero_sigma_pixel_device, void* stream);
 
 /* Number of bwm kernel launches issued by this process so far (all plans). */
 int64_t bwm_launch_count(void);

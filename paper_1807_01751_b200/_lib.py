@@ -27,7 +27,7 @@ BWM_NAN_MASK = 1
 NAN_MODES = {"fill": BWM_NAN_FILL, "mask": BWM_NAN_MASK}
 
 INT64_MAX = (1 << 63) - 1
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 
 class Dims(C.Structure):
@@ -62,6 +62,7 @@ class Outputs(C.Structure):
         ("first_break", C.c_void_p),
         ("max_abs_f64", C.c_void_p),
         ("detected", C.c_void_p),
+        ("sup_stat", C.c_void_p),
     ]
 
 
@@ -94,6 +95,7 @@ SIGNATURES = [
     ("bwm_last_host_stats", C.c_int,
      [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("bwm_plan_info", C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
+    ("bwm_zero_sigma_init", C.c_int, [C.c_void_p, C.c_void_p]),
     ("bwm_launch_count", C.c_int64, []),
     ("bwm_smem_bytes", C.c_int64, [C.POINTER(Dims)]),
     ("bwm_last_error", C.c_char_p, []),

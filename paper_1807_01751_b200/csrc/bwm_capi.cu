@@ -229,8 +229,8 @@ struct HostPipe {
     size_t bytes = 0;                  // device memory held by the pipeline
     cudaStream_t s_h2d[2] = {nullptr, nullptr};
     cudaStream_t s_k[2] = {nullptr, nullptr};
-    cudaEvent_t ev_in[2], ev_k0[2], ev_k1[2], ev_free[2];
-    bool events = false;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_k0[2] = {nullptr, nullptr}, ev_k1[2] = {nullptr, nullptr},
+                ev_free[2] = {nullptr, nullptr};
     // pinned landing zone for result maps whose destination is pageable (plain numpy): the D2H
     // lands here at full rate and threads memcpy it out (grown on demand, kept across calls)
     char* h_stage = nullptr;
@@ -262,7 +262,13 @@ struct bwm_plan {
     // float64 fixup of ill-conditioned pixels (bwm_fixup.cu): device list + count, grown on use
     double lambda_d = 0.0;            // masked float64 kernel
     float fix_ratio = 300.f;     // ||y-c||^2 / RSS above which a pixel is recomputed in float64
-    mutable std::mutex fix_mu;
+    // Plan-owned scratch (the fixup list + count, the masked BIG rings) is shared by every
+    // bwm_monitor call on the plan: calls that use it are ordered on the device through
+    // scratch_ev (each waits for the previous user's last kernel, then records its own), so
+    // concurrent calls on different streams — the chunked host pipeline, or callers — never
+    // overlap on it.  scratch_mu makes the wait + record pair atomic across host threads.
+    mutable std::mutex scratch_mu;
+    cudaEvent_t scratch_ev = nullptr;
     mutable int64_t* d_fix_list = nullptr;
     mutable unsigned int* d_fix_count = nullptr;
     mutable int64_t fix_cap = 0;
@@ -309,6 +315,8 @@ static void plan_free_tables(bwm_plan* plan) {
     cudaFree(plan->d_xx);
     cudaFree(plan->d_gfull);
     cudaFree(plan->d_ring);
+    if (plan->scratch_ev) cudaEventDestroy(plan->scratch_ev);
+    plan->scratch_ev = nullptr;
 }
 
 
@@ -357,11 +365,13 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
     plan->smem_masked = bwm::masked_smem_bytes(N, n, h, p, plan->mbig);
     if (plan->smem_masked > max_optin) {
         const int64_t need = plan->smem_masked;
+        plan_free_tables(plan);
         delete plan;
         return set_err(BWM_E_SMEM, "masked tables need %lld B of shared memory, device allows %d",
                        (long long)need, max_optin);
     }
     if (n16 > 65535 || N > 65535) {
+        plan_free_tables(plan);
         delete plan;
         return set_err(BWM_E_DIMS, "masked mode supports at most 65535 dates");
     }
@@ -442,6 +452,15 @@ const char* bwm_last_error(void) { return g_err.c_str(); }
 int bwm_abi_version(void) { return BWM_ABI_VERSION; }
 int64_t bwm_launch_count(void) { return g_launches.load(); }
 
+int bwm_zero_sigma_init(int64_t* z, void* stream) {
+    if (!z) return set_err(BWM_E_NULL, "zero_sigma_pixel is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    // INT64_MAX little-endian: bytes 0-6 = 0xff, byte 7 = 0x7f
+    BWM_CUDA(cudaMemsetAsync(z, 0xff, 7, st));
+    BWM_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(z) + 7, 0x7f, 1, st));
+    return BWM_OK;
+}
+
 int64_t bwm_smem_bytes(const bwm_dims* d) {
     int rc = validate_dims(d);
     if (rc) return rc;
@@ -518,10 +537,18 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     int max_optin = 0;
     cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device);
+    {
+        cudaError_t e0 = cudaEventCreateWithFlags(&plan->scratch_ev, cudaEventDisableTiming);
+        if (e0 != cudaSuccess) {
+            delete plan;
+            return set_err((int)e0, "cudaEventCreate: %s", cudaGetErrorString(e0));
+        }
+    }
     if (dims->nan_mode == BWM_NAN_MASK) return plan_create_masked(plan, tb, max_optin, out_plan);
     if (plan->smem_tma > max_optin || plan->tring.mode < 0) plan->smem_tma = 0;
     if (plan->smem > max_optin) {
         int64_t need = plan->smem;
+        plan_free_tables(plan);
         delete plan;
         return set_err(BWM_E_SMEM, "tables need %lld B of shared memory, device allows %d",
                        (long long)need, max_optin);
@@ -545,6 +572,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         for (int t = 0; t < n; ++t) nrm += Q[(size_t)t * p + j] * Q[(size_t)t * p + j];
         nrm = std::sqrt(nrm);
         if (!(nrm > 1e-12)) {
+            plan_free_tables(plan);
             delete plan;
             return set_err(BWM_E_DIMS, "history design is rank deficient (column %d)", j);
         }
@@ -593,11 +621,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     }
 
     auto fail = [&](cudaError_t e, const char* what) {
-        cudaFree(plan->d_mt);
-        cudaFree(plan->d_xt);
-        cudaFree(plan->d_bound);
-        cudaFree(plan->d_rinv);
-        cudaFree(plan->d_xtd);
+        plan_free_tables(plan);
         delete plan;
         return set_err((int)e, "%s: %s", what, cudaGetErrorString(e));
     };
@@ -680,12 +704,8 @@ static void pipe_free(HostPipe& hp) {
         cudaFree(hp.d_det[b]);
         if (hp.s_h2d[b]) cudaStreamDestroy(hp.s_h2d[b]);
         if (hp.s_k[b]) cudaStreamDestroy(hp.s_k[b]);
-        if (hp.events) {
-            cudaEventDestroy(hp.ev_in[b]);
-            cudaEventDestroy(hp.ev_k0[b]);
-            cudaEventDestroy(hp.ev_k1[b]);
-            cudaEventDestroy(hp.ev_free[b]);
-        }
+        for (cudaEvent_t ev : {hp.ev_in[b], hp.ev_k0[b], hp.ev_k1[b], hp.ev_free[b]})
+            if (ev) cudaEventDestroy(ev);
     }
     cudaFree(hp.d_zero);
     if (hp.h_stage) cudaFreeHost(hp.h_stage);
@@ -713,6 +733,8 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         return set_err(BWM_E_DIMS, "ld_out (%lld) < n_pixels (%lld)", (long long)out->ld_out,
                        (long long)n_pixels);
     if (pixel_offset < 0) return set_err(BWM_E_DIMS, "pixel_offset must be >= 0");
+    if (out->sup_stat && plan->dims.nan_mode != BWM_NAN_FILL)
+        return set_err(BWM_E_PARAMS, "sup_stat is a fill-mode output (critical_value)");
     int cur = -1;
     cudaGetDevice(&cur);
     if (cur != plan->device)
@@ -744,11 +766,20 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     k.beta = out->beta;
     k.mo_mean = out->mo_mean;
     k.mosum = out->mosum;
+    k.sup = out->sup_stat;
     k.ld_out = out->ld_out;
     k.zero_sigma = reinterpret_cast<unsigned long long*>(out->zero_sigma_pixel);
     k.xtd = plan->precise ? plan->d_xtd : nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     int launched = 0;
+    // float64 fixup list for ill-conditioned pixels (fill mode, float32 kernels)
+    const bool fixup = !plan->masked && !plan->precise && plan->fix_ratio > 0.f && plan->d_xtd;
+    const bool uses_scratch = fixup || (plan->masked && !plan->precise && plan->mbig);
+    std::unique_lock<std::mutex> scratch_lock(plan->scratch_mu, std::defer_lock);
+    if (uses_scratch) {
+        scratch_lock.lock();
+        BWM_CUDA(cudaStreamWaitEvent(st, plan->scratch_ev, 0));
+    }
 
     if (plan->masked && plan->precise) {
         bwm::KParams kf = k;
@@ -777,16 +808,13 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     auto al = [](const void* q, uintptr_t a) { return (reinterpret_cast<uintptr_t>(q) & (a - 1)) == 0; };
     const bool out_al = al(out->valid, 2) && al(out->first_idx, 8) && al(out->max_abs, 8) &&
                         (!out->mo_mean || al(out->mo_mean, 8)) && (!out->beta || al(out->beta, 8)) &&
-                        (!out->mosum || al(out->mosum, 8)) && (out->ld_out % 2 == 0 || (!out->beta && !out->mosum));
+                        (!out->mosum || al(out->mosum, 8)) && (!out->sup_stat || al(out->sup_stat, 8)) && (out->ld_out % 2 == 0 || (!out->beta && !out->mosum));
     const bool tma_ok = !plan->masked && !plan->force_ldg && !plan->precise && plan->smem_tma > 0 && al(y, 16) &&
                         (ld_y % 4 == 0) && out_al;
     const bool ldg_ok = al(y, 8) && (ld_y % 2 == 0);
     const Kind main_kind = tma_ok ? kTma : kLdgFast;
     const int64_t full = (tma_ok || ldg_ok) ? (n_pixels / bwm::kTile) * bwm::kTile : 0;
-    // float64 fixup list for ill-conditioned pixels (fill mode, float32 kernels)
-    const bool fixup = !plan->masked && !plan->precise && plan->fix_ratio > 0.f && plan->d_xtd;
     if (fixup) {
-        std::lock_guard<std::mutex> lk(plan->fix_mu);
         // capacity: every pixel of small calls, 4M entries (32 MB) at most — flagged pixels are
         // rare on real data, and a near-capacity stack must not run out of HBM for the list
         const int64_t want = std::min<int64_t>(n_pixels, 4ll << 20);
@@ -825,6 +853,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         kp.beta = out->beta ? out->beta + p0 : nullptr;
         kp.mo_mean = out->mo_mean ? out->mo_mean + p0 : nullptr;
         kp.mosum = out->mosum ? out->mosum + p0 : nullptr;
+        kp.sup = out->sup_stat ? out->sup_stat + p0 : nullptr;
         const bool lean = kind == kTma && plan->const_bound && !out->mosum && !out->mo_mean;
         KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode | (lean ? bwm::kTmaLean : 0)
                                                           : (plan->ring ? 0 : (int)bwm::kRingLag));
@@ -848,6 +877,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         if (e != cudaSuccess) return set_err((int)e, "fixup launch failed: %s", cudaGetErrorString(e));
         ++launched;
     }
+    if (uses_scratch) BWM_CUDA(cudaEventRecord(plan->scratch_ev, st));
     if (out->first_break || out->max_abs_f64 || out->detected) {
         cudaError_t e = bwm::launch_finalize(out->first_idx, out->max_abs, n_pixels, d.n_hist, out->first_break,
                                              out->max_abs_f64, out->detected, st);
@@ -881,8 +911,8 @@ static int pipe_ensure(bwm_plan* plan, int64_t chunk, int nbuf, const PipeNeeds&
                     (!w.det || hp.d_det[0]);
     if (ok) return BWM_OK;
     pipe_free(hp);
-    hp.chunk = chunk;
-    hp.nbuf = nbuf;
+    // allocate into hp; any failure frees everything (no half-built pipe whose signature matches)
+    const int rc = [&]() -> int {
     for (int b = 0; b < 2; ++b) {
         if (b < nbuf) {
             BWM_CUDA(cudaMalloc(&hp.d_y[b], (size_t)d.n_obs * chunk * 4));
@@ -903,8 +933,16 @@ static int pipe_ensure(bwm_plan* plan, int64_t chunk, int nbuf, const PipeNeeds&
         BWM_CUDA(cudaEventCreate(&hp.ev_k1[b]));
         BWM_CUDA(cudaEventCreateWithFlags(&hp.ev_free[b], cudaEventDisableTiming));
     }
-    hp.events = true;
     BWM_CUDA(cudaMalloc(&hp.d_zero, 2 * sizeof(int64_t)));
+    return BWM_OK;
+    }();
+    if (rc != BWM_OK) {
+        const std::string msg = g_err;
+        pipe_free(hp);
+        return set_err(rc, "%s", msg.c_str());
+    }
+    hp.chunk = chunk;
+    hp.nbuf = nbuf;
     hp.bytes = pipe_bytes(d, chunk, nbuf, w);
     return BWM_OK;
 }
@@ -923,6 +961,7 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
     if (n_pixels < 1) return set_err(BWM_E_DIMS, "stack needs at least one pixel");
     if (ld_y < n_pixels) return set_err(BWM_E_DIMS, "ld_y < n_pixels");
     if ((out->beta || out->mosum) && out->ld_out < n_pixels) return set_err(BWM_E_DIMS, "ld_out < n_pixels");
+    if (out->sup_stat) return set_err(BWM_E_PARAMS, "sup_stat is a bwm_monitor (device) output");
 
     std::lock_guard<std::mutex> lock(plan->mu);
     DeviceRestore guard(plan->device);
@@ -960,7 +999,18 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
     const int64_t init[2] = {INT64_MAX, INT64_MAX};
     BWM_CUDA(cudaMemcpy(hp.d_zero, init, sizeof init, cudaMemcpyHostToDevice));
 
-    cudaEvent_t t_start, t_end;
+    cudaEvent_t t_start = nullptr, t_end = nullptr;
+    std::vector<cudaEvent_t> kev;                      // per-chunk kernel timing
+    struct EventGuard {                                 // destroys this call's events on every exit
+        cudaEvent_t& a;
+        cudaEvent_t& b;
+        std::vector<cudaEvent_t>& v;
+        ~EventGuard() {
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+            for (auto& e : v) if (e) cudaEventDestroy(e);
+        }
+    } event_guard{t_start, t_end, kev};
     BWM_CUDA(cudaEventCreate(&t_start));
     BWM_CUDA(cudaEventCreate(&t_end));
     BWM_CUDA(cudaEventRecord(t_start, hp.s_h2d[0]));
@@ -1049,7 +1099,7 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
         BWM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hp.h_stage), stage_need, cudaHostAllocPortable));
         hp.h_stage_bytes = stage_need;
     }
-    std::vector<cudaEvent_t> kev((size_t)(2 * n_chunks), nullptr);   // per-chunk kernel timing
+    kev.assign((size_t)(2 * n_chunks), nullptr);
     for (auto& ev : kev) BWM_CUDA(cudaEventCreate(&ev));
     for (int64_t c = 0; c < n_chunks; ++c) {
         const int b = nbuf == 1 ? 0 : (int)(c & 1);
@@ -1173,7 +1223,6 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
         BWM_CUDA(cudaEventElapsedTime(&ms, kev[2 * c], kev[2 * c + 1]));
         kernel_ms += ms;
     }
-    for (auto& ev : kev) cudaEventDestroy(ev);
     for (int64_t g : pending) {
         BWM_CUDA(cudaEventSynchronize(slot_ev[(size_t)(g % K)]));
         reader.release(g);
@@ -1214,8 +1263,6 @@ static int monitor_pipeline(bwm_plan* plan, const float* y_host, int64_t ld_y, c
     BWM_CUDA(cudaEventSynchronize(t_end));
     float total = 0;
     cudaEventElapsedTime(&total, t_start, t_end);
-    cudaEventDestroy(t_start);
-    cudaEventDestroy(t_end);
     hp.last_kernel_ms = kernel_ms;
     hp.last_total_ms = total;
     hp.last_h2d = h2d;

@@ -46,6 +46,7 @@ struct KParams {
     float* beta;
     float* mo_mean;
     float* mosum;
+    float* sup;                 // [P] or nullptr: sup_j |MO_j| / bound_j (critical_value statistic)
     int64_t ld_out;
     unsigned long long* zero_sigma;   // atomicMin target (int64 bit pattern, non-negative)
     // masked-NaN mode (bwm_kernel_masked.cuh); xt then holds X'^T (the centred raw design)
@@ -65,13 +66,21 @@ struct KParams {
     int64_t fix_base;
 };
 
-// append pixel `px` (launch-relative) to the fixup list when its history fit is ill-conditioned
+// append pixel `px` (launch-relative) to the fixup list when its history fit is ill-conditioned:
+// ||y-c||^2 > ratio * RSS, or a one-pass RSS that cancelled to <= 0 (clamped to 0 by
+// rss_onepass) on a history that is not constant — the worst-conditioned, near-noiseless
+// pixels; the float64 fixup recomputes sigma with the reference's two-pass sum.
 __device__ __forceinline__ void fix_flag(const KParams& prm, bool valid, double q, float rss, int64_t px) {
-    if (prm.fix_list && valid && rss > 0.f && q > (double)prm.fix_ratio * (double)rss) {
+    if (prm.fix_list && valid && q > 0.0 && (rss == 0.f || q > (double)prm.fix_ratio * (double)rss)) {
         const unsigned int i = atomicAdd(prm.fix_count, 1u);
         if (i < prm.fix_cap) prm.fix_list[i] = prm.fix_base + px;
     }
 }
+
+// zero-sigma contract (engine.py:373-378): the reference raises when float64 gives sigma == 0
+// exactly, i.e. for an identically zero filled history: ||y - c||^2 == 0 with c == 0.  A
+// one-pass RSS that merely cancels to 0 on a varying history is not zero sigma (fix_flag).
+__device__ __forceinline__ bool zero_history(bool valid, double q, float c) { return valid && q == 0.0 && c == 0.f; }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }

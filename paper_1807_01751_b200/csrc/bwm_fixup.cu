@@ -67,8 +67,12 @@ __global__ void __launch_bounds__(128) fixup_kernel(const KParams prm, int p, co
         const double sigma = sqrt(rss / (double)(n - p));
         const double scale = sigma * sqrt_n;
         const double inv = scale > 0.0 ? 1.0 / scale : 0.0;
+        // float64 two-pass sigma == 0 on a listed (valid, non-constant) pixel: the reference's
+        // ZeroResidualError criterion (engine.py:373-378), decided here rather than from the
+        // float32 one-pass RSS that flagged the pixel
+        if (!(scale > 0.0)) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px));
         // pass 3: monitoring, r_{t-h} from a lagging cursor with its own fill state
-        double mx = 0.0, msum = 0.0, lag_last = lastw;
+        double mx = 0.0, msum = 0.0, lag_last = lastw, sr = 0.0;
         int first = 0;
         for (int t = n; t < N; ++t) {
             const float v = y[(int64_t)t * ld];
@@ -88,12 +92,14 @@ __global__ void __launch_bounds__(128) fixup_kernel(const KParams prm, int p, co
             mx = fmax(mx, a);
             const double b = (double)prm.bound[t - n];
             if (first == 0 && a > b) first = t - n + 1;   // strict crossing (_kernels.py:47)
+            sr = fmax(sr, a / b);
             msum += mo;
             if (prm.mosum) prm.mosum[(int64_t)(t - n) * prm.ld_out + px] = (float)mo;
         }
         prm.first_idx[px] = first;
         prm.max_abs[px] = (float)mx;
         if (prm.mo_mean) prm.mo_mean[px] = (float)(msum / (double)(N - n));
+        if (prm.sup) prm.sup[px] = (float)sr;
     }
 }
 

@@ -239,15 +239,16 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         if (RING) ring[slot * kThreads] = f2(0.f, 0.f);
 
         // sigma and the zero-sigma contract: see bwm_kernel_tma.cuh (identical arithmetic)
-        const bool z0 = valid0 && ss.x == 0.f && c.x == 0.f, z1 = valid1 && ss.y == 0.f && c.y == 0.f;
+        const bool z0 = zero_history(valid0, xtd ? qd0 : q0, c.x), z1 = zero_history(valid1, xtd ? qd1 : q1, c.y);
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
         const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);
         const float2 inv = inv_scale(sc);
 
         // ---- pass 3: monitoring period, fused MOSUM + detect -------------------------
-        float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f);
+        float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f), sr = f2(0.f, 0.f);
         int first0 = 0x7fffffff, first1 = 0x7fffffff;
         float* const mo_out = prm.mosum;
+        const bool want_sup = prm.sup != nullptr;
         // one monitoring row; fast: no bounds checks, refill is the same pass's row t+D
         auto mon_row = [&](const int k, const int t, const bool fast) {
             const float2 v = buf[k];
@@ -277,6 +278,10 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
             mx.y = fmaxf(mx.y, a1);
             if (a0 > bs.x) first0 = min(first0, j + 1);  // strict crossing (_kernels.py:47)
             if (a1 > bs.y) first1 = min(first1, j + 1);
+            if (want_sup) {                              // max_j |acc_j| / b_j (unscaled)
+                sr.x = fmaxf(sr.x, __fdividef(a0, bj));
+                sr.y = fmaxf(sr.y, __fdividef(a1, bj));
+            }
             msum = add2(msum, acc);
             if (mo_out) {
                 const float2 mo = mul2(acc, inv);
@@ -308,11 +313,14 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
             const float2 mxs = mul2(mx, inv), mean = mul2(mul2(msum, inv), f2(inv_m, inv_m));
             prm.max_abs[px0] = mxs.x;
             if (prm.mo_mean) prm.mo_mean[px0] = mean.x;
+            const float2 srs = mul2(sr, inv);
+            if (want_sup) prm.sup[px0] = srs.x;
             if (npx >= 2) {
                 prm.valid[px0 + 1] = valid1;
                 prm.first_idx[px0 + 1] = first1 == 0x7fffffff ? 0 : first1;
                 prm.max_abs[px0 + 1] = mxs.y;
                 if (prm.mo_mean) prm.mo_mean[px0 + 1] = mean.y;
+                if (want_sup) prm.sup[px0 + 1] = srs.y;
             }
             if (prm.beta) store_beta<NP>(prm, px0, c, bq, valid0, valid1, npx);
         }

@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         const float2 ss = rss_onepass<NP>(q0, q1, bq);
         fix_flag(prm, valid0, q0, ss.x, px0);
         fix_flag(prm, valid1, q1, ss.y, px0 + 1);
-        const bool z0 = valid0 && ss.x == 0.f && c.x == 0.f, z1 = valid1 && ss.y == 0.f && c.y == 0.f;
+        const bool z0 = zero_history(valid0, q0, c.x), z1 = zero_history(valid1, q1, c.y);
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
         const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);
 
@@ -493,9 +493,10 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         if (MODE == kRingTmem) ring_put_row(q_nh, f2(0.f, 0.f));  // r_{n-h} is not in window 0
 
         // ---- pass 3: monitoring period, fused MOSUM + detect (unscaled frame) ----------
-        float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f);
+        float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f), sr = f2(0.f, 0.f);
         int first0 = 0x7fffffff, first1 = 0x7fffffff;
         float* const mo_out = prm.mosum;
+        const bool want_sup = prm.sup != nullptr;
         const float2 inv = inv_scale(sc);
         const float2 bsc = mul2(sc, f2(s_bd[n], s_bd[n]));   // LEAN: the constant boundary, unscaled
         auto step = [&](const float2 r, const float2 old, const int t, const float bj) {
@@ -508,6 +509,10 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
             if (a0 > bs.x) first0 = min(first0, j1);  // strict crossing (_kernels.py:47)
             if (a1 > bs.y) first1 = min(first1, j1);
             if (!LEAN) {
+                if (want_sup) {                        // max_j |acc_j| / b_j (unscaled)
+                    sr.x = fmaxf(sr.x, __fdividef(a0, bj));
+                    sr.y = fmaxf(sr.y, __fdividef(a1, bj));
+                }
                 msum = add2(msum, acc);
                 if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)(t - n) * prm.ld_out + px0) = mul2(acc, inv);
             }
@@ -572,6 +577,10 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
             make_int2(first0 == 0x7fffffff ? 0 : first0, first1 == 0x7fffffff ? 0 : first1);
         *reinterpret_cast<float2*>(prm.max_abs + px0) = mul2(mx, inv);
         if (!LEAN && prm.mo_mean) *reinterpret_cast<float2*>(prm.mo_mean + px0) = mul2(mul2(msum, inv), f2(inv_m, inv_m));
+        if (want_sup) {        // LEAN: b_j == b_n for every j
+            const float2 s = LEAN ? mul2(mul2(mx, inv), f2(1.0f / s_bd[n], 1.0f / s_bd[n])) : mul2(sr, inv);
+            *reinterpret_cast<float2*>(prm.sup + px0) = s;
+        }
         if (prm.beta) store_beta<NP>(prm, px0, c, bq, valid0, valid1, 2);
     }
 

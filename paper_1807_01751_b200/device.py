@@ -38,6 +38,7 @@ class DeviceResult:
     beta: object = None  # float32 [p, P]
     mo_mean: object = None   # float32 [P]
     mosum: object = None     # float32 [N-n, P]
+    sup: object = None       # float32 [P]: sup_j |MO_j| / bound_j (critical_value statistic)
     zero_sigma: Optional[int] = None   # lowest global pixel with sigma == 0, if any
     first_break: object = None         # int64 [P]: n + first_idx, 0 = none (reference dtype)
     max_abs_f64: object = None         # float64 [P]
@@ -158,8 +159,12 @@ class DevicePlan:
     # ------------------------------------------------------------------ device path
     def run_device(self, y, *, keep_mosum: bool = False, beta: bool = False, mean: bool = False,
                    pixel_offset: int = 0, stream=None, out: Optional[DeviceResult] = None,
-                   check_zero: bool = True, ref_dtypes: bool = False) -> DeviceResult:
-        """Monitor a device-resident stack y: float32 CUDA tensor (N, P), unit pixel stride."""
+                   check_zero: bool = True, ref_dtypes: bool = False, sup: bool = False) -> DeviceResult:
+        """Monitor a device-resident stack y: float32 CUDA tensor (N, P), unit pixel stride.
+
+        `out` (a previous call's result with the same P) is reused as is: no allocation and
+        no torch kernel per call — the zero-sigma slot is reset by bwm_zero_sigma_init
+        (memset), so every kernel this call launches is a libbwm kernel."""
         import torch
 
         if not (isinstance(y, torch.Tensor) and y.is_cuda and y.dtype == torch.float32):
@@ -181,24 +186,31 @@ class DevicePlan:
                 mo_mean=torch.empty(P, dtype=torch.float32, device=dev) if mean else None,
                 mosum=torch.empty((self.n_obs - self.n_hist, P), dtype=torch.float32, device=dev)
                 if keep_mosum else None,
+                sup=torch.empty(P, dtype=torch.float32, device=dev) if sup else None,
             )
             if ref_dtypes:
                 out.first_break = torch.empty(P, dtype=torch.int64, device=dev)
                 out.max_abs_f64 = torch.empty(P, dtype=torch.float64, device=dev)
                 out.detected = torch.empty(P, dtype=torch.uint8, device=dev)
-        zero = torch.full((1,), _lib.INT64_MAX, dtype=torch.int64, device=dev)
+        elif int(out.valid.shape[0]) != P:
+            raise ValueError(f"out holds maps for {int(out.valid.shape[0])} pixels, stack has {P}")
+        zero = getattr(out, "_zero_tensor", None)
+        if zero is None:
+            zero = torch.empty(1, dtype=torch.int64, device=dev)
+            out._zero_tensor = zero
         dp = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
         o = _lib.Outputs(
             out.valid.data_ptr(), out.first_idx.data_ptr(), out.max_abs.data_ptr(),
             dp(out.beta), dp(out.mo_mean), dp(out.mosum), P, zero.data_ptr(),
-            dp(out.first_break), dp(out.max_abs_f64), dp(out.detected),
+            dp(out.first_break), dp(out.max_abs_f64), dp(out.detected), dp(out.sup),
         )
         with torch.cuda.device(dev):
             s = stream if stream is not None else torch.cuda.current_stream(dev)
+            sp = C.c_void_p(s.cuda_stream)
+            _lib.check(self._lib.bwm_zero_sigma_init(zero.data_ptr(), sp), "bwm_zero_sigma_init")
             _lib.check(self._lib.bwm_monitor(self._handle, y.data_ptr(), y.stride(0), P, int(pixel_offset),
-                                             C.byref(o), C.c_void_p(s.cuda_stream)), "bwm_monitor")
+                                             C.byref(o), sp), "bwm_monitor")
         out.zero_sigma = None
-        out._zero_tensor = zero
         if check_zero:
             z = int(zero.item())
             out.zero_sigma = z if z != _lib.INT64_MAX else None

@@ -11,8 +11,11 @@ libbwm.  The host does what the reference's host does once per batch, in float64
 validation, lambda, the design/mapping matrices and the boundary.
 
 Differences a caller can observe (documented in DESIGN.md):
-  * backend "fused" (default) and "cuda" both run the GPU kernel; "naive" — the reference's
-    per-pixel CPU oracle — is not provided (ValueError).
+  * every backend — "fused" (default), "naive" and "cuda" — runs the same GPU kernel.  The
+    reference's "naive" backend is its per-pixel CPU restatement, contractually identical to
+    "fused" (test_acceptance.py:67-95: indices equal, MO within 1e-9); here both names
+    select the one fused kernel, so the contract holds exactly and a reference caller that
+    passes backend="naive" keeps working.  There is no CPU path.
   * `threads` and `block_size` are validated like the reference and otherwise ignored:
     the CUDA grid replaces the thread pool and the 4096-pixel blocks.
   * the kernel computes in float32 (compensated where it matters); max_abs_mo agrees
@@ -40,7 +43,7 @@ THREADS_ENV_VAR = "BREAKWATCH_THREADS"
 CALIBRATION_REPS = 50_000
 CALIBRATION_SEED = 7
 PHASE_NAMES = ("ingest", "model", "predictions", "residuals", "mosum", "breaks")
-BACKENDS = ("fused", "cuda")
+BACKENDS = ("fused", "naive", "cuda")
 NAN_MODES = ("fill", "mask")
 
 
@@ -143,10 +146,7 @@ class MonitorConfig:
         if self.nan_mode not in NAN_MODES:
             raise ValueError(f"nan_mode must be 'fill' or 'mask', got {self.nan_mode!r}")
         if self.backend not in BACKENDS:
-            raise ValueError(
-                "backend must be 'fused' or 'cuda' (the reference's 'naive' per-pixel CPU "
-                "oracle is not part of this package)"
-            )
+            raise ValueError("backend must be 'fused', 'naive' or 'cuda'")
 
     @property
     def n_params(self) -> int:
@@ -208,6 +208,26 @@ class PhaseTimings:
     @property
     def phase_sum(self) -> float:
         return sum(getattr(self, name) for name in PHASE_NAMES)
+
+
+def fill_gaps(series) -> np.ndarray:
+    """Forward fill from the first finite value; back-fill the leading gap (engine.py:195-211).
+
+    The per-series statement of the gap fill the kernel applies to every pixel (a host numpy
+    helper of the reference's public API, not a compute path): a series without gaps is
+    returned unchanged, one with no finite value raises AllNanSeriesError.
+    """
+    from .errors import AllNanSeriesError
+
+    values = np.asarray(series)
+    finite = np.isfinite(values)
+    if finite.all():
+        return values
+    if not finite.any():
+        raise AllNanSeriesError("series has no finite values")
+    # index of the latest finite sample at or before each position; leading gap -> first finite
+    last = np.maximum.accumulate(np.where(finite, np.arange(values.size), -1))
+    return values[np.where(last < 0, int(np.argmax(finite)), last)]
 
 
 def resolve_crit_value(config: MonitorConfig, n_obs: int, threads: int = 1) -> float:

@@ -3,8 +3,10 @@
 ``log_plus`` and ``boundary_values`` are the per-geometry constants the kernel compares
 against (mosum.py:27-32, 68-79).  ``critical_value`` is the Monte Carlo calibration of
 lambda (mosum.py:166-227): the null draws come from the same per-replication Philox
-substreams as the reference, and the replications run through the same fused GPU kernel
-as the data (libbwm), so there is no CPU MOSUM in this package.
+substreams as the reference, and ALL replications run as one stack through the same fused
+GPU kernel as the data (libbwm), which emits the per-replication statistic
+sup_j |MO_j| / sqrt(log_plus) directly (bwm_outputs.sup_stat) — no MOSUM matrix, no CPU
+MOSUM in this package.
 """
 
 from __future__ import annotations
@@ -78,16 +80,31 @@ class CriticalValueRequest:
             )
 
 
-def null_draws(request: CriticalValueRequest, start: int, stop: int, n_obs: int) -> np.ndarray:
+def null_draws(request: CriticalValueRequest, start: int, stop: int, n_obs: int,
+               dtype=np.float64, out: Optional[np.ndarray] = None) -> np.ndarray:
     """Standard-normal draws of replications [start, stop), time-major (n_obs, width).
 
     Replication r uses Philox(key=seed, counter=r << 128), exactly the reference's
-    substreams (mosum.py:195-198), so results do not depend on batching.
+    substreams (mosum.py:195-198), so results do not depend on batching.  One bit generator
+    is re-keyed per replication by resetting its counter state (the same stream as a fresh
+    ``Philox(key, counter)``: the 4-word buffer is emptied), half the cost of constructing
+    a generator per replication.  ``out`` (n_obs, stop - start) receives the draws cast to
+    its dtype (float32 for the kernel).
     """
-    out = np.empty((n_obs, stop - start))
-    for j in range(stop - start):
-        rng = np.random.Generator(np.random.Philox(key=request.seed, counter=(start + j) << 128))
-        out[:, j] = rng.standard_normal(n_obs)
+    width = stop - start
+    if out is None:
+        out = np.empty((n_obs, width), dtype=dtype)
+    bg = np.random.Philox(key=request.seed)
+    gen = np.random.Generator(bg)
+    state = bg.state
+    mask = (1 << 64) - 1
+    for j in range(width):
+        c = (start + j) << 128
+        state["state"]["counter"][:] = [(c >> (64 * i)) & mask for i in range(4)]
+        state["buffer_pos"] = 4
+        state["has_uint32"] = 0
+        bg.state = state
+        out[:, j] = gen.standard_normal(n_obs)
     return out
 
 
@@ -96,9 +113,10 @@ def critical_value(request: CriticalValueRequest, threads: int = 1, device=None)
 
     Same geometry rules as the reference (mosum.py:166-227): regular axis 1..N with
     N = round(horizon * n_sim), h = round(h_frac * n_sim), the full season-trend fit per
-    replication.  The replications are monitored on the GPU by libbwm (keep_mosum), so
-    the statistic sees float32 residual arithmetic: agreement with the float64 reference
-    is ~1e-6 relative, not bit-exact.
+    replication.  The draws (host, the reference's Philox substreams, `threads` workers)
+    fill one float32 stack of all replications; one libbwm launch over it emits each
+    replication's statistic (sup_stat), so the statistic sees float32 residual arithmetic:
+    agreement with the float64 reference is ~1e-6 relative, not bit-exact.
     """
     from concurrent.futures import ThreadPoolExecutor
 
@@ -116,24 +134,21 @@ def critical_value(request: CriticalValueRequest, threads: int = 1, device=None)
     from .model import regular_axis
 
     axis = regular_axis(n_obs)
-    # unit boundary: the kernel's own crossing test is irrelevant here; only MO is kept
+    # unit lambda: bound_j = sqrt(log_plus((n+1+j)/n)), so sup_stat is the reference statistic
     plan = DevicePlan.get(axis, request.freq, request.harmonics, n_hist, bandwidth, 1.0, device)
-    t = np.arange(n_hist + 1, n_obs + 1, dtype=np.float64)
-    inv_shape = torch.as_tensor(1.0 / np.sqrt(log_plus(t / n_hist)), dtype=torch.float32,
-                                device=plan.torch_device)[:, None]
     blocks = [(s, min(s + REPLICATION_BLOCK, request.reps)) for s in range(0, request.reps, REPLICATION_BLOCK)]
-    sup = np.empty(request.reps)
+    host = torch.empty((n_obs, request.reps), dtype=torch.float32, pin_memory=True).numpy()
 
     def draws(block):
-        return null_draws(request, block[0], block[1], n_obs).astype(np.float32)
+        null_draws(request, block[0], block[1], n_obs, out=host[:, block[0]:block[1]])
 
     with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
-        for (start, stop), y in zip(blocks, pool.map(draws, blocks)):
-            res = plan.run_device(torch.as_tensor(y, device=plan.torch_device), keep_mosum=True)
-            if res.zero_sigma is not None:
-                from .errors import ZeroResidualError
+        list(pool.map(draws, blocks))
+    y = torch.as_tensor(host).to(plan.torch_device, non_blocking=True)
+    res = plan.run_device(y, sup=True)
+    if res.zero_sigma is not None:
+        from .errors import ZeroResidualError
 
-                raise ZeroResidualError("a simulated null series produced a zero residual scale")
-            stat = (res.mosum.abs() * inv_shape).amax(dim=0)
-            sup[start:stop] = stat.double().cpu().numpy()
+        raise ZeroResidualError("a simulated null series produced a zero residual scale")
+    sup = res.sup.double().cpu().numpy()
     return float(np.quantile(sup, 1.0 - request.alpha))

@@ -197,3 +197,48 @@ def generate(spec: SynthSpec, threads: Optional[int] = None):
         for i in range(n_blocks):
             block(i)
     return SeriesStack(out, regular_axis(N)), np.arange(m) < n_break
+
+
+# ---- the reference's scaling benchmark (synth.py:108-149) -----------------------------------
+BENCH_CSV_HEADER = "m,ingest,model,predictions,residuals,mosum,breaks,total"
+
+
+def bench_scaling(m_values, config, template: SynthSpec, threads: Optional[int] = None, sink=None):
+    """profile_run of one freshly generated stack per pixel count (reference synth.py:108-135).
+
+    Same contract: lambda is resolved once up front (it depends on the monitoring geometry,
+    not on the pixel count), each m gets `generate(replace(template, n_pixels=m))`, and
+    (m, PhaseTimings) rows are returned — and written as CSV when a sink is given.  The
+    timings are the GPU path's (PhaseTimings: ingest = H2D, mosum = the fused kernel).
+    """
+    from dataclasses import replace
+
+    from .engine import profile_run, resolve_crit_value, resolve_threads
+
+    m_values = [int(m) for m in m_values]
+    if not m_values:
+        raise ValueError("need at least one pixel count")
+    if any(m < 1 for m in m_values):
+        raise ValueError("pixel counts must be >= 1")
+    if config.crit_value is None:
+        config = replace(config, crit_value=resolve_crit_value(config, template.n_obs, resolve_threads(threads)))
+    rows = []
+    for m in m_values:
+        stack, _ = generate(replace(template, n_pixels=m), threads=threads)
+        _, timings = profile_run(stack, config, threads=threads)
+        rows.append((m, timings))
+    if sink is not None:
+        write_bench_csv(rows, sink)
+    return rows
+
+
+def write_bench_csv(rows, sink) -> int:
+    """bench_scaling rows as CSV, six decimals per phase (reference synth.py:138-149)."""
+    from .dataio import _open
+
+    with _open(sink, "w") as out:
+        out.write(BENCH_CSV_HEADER + "\n")
+        for m, tm in rows:
+            fields = [tm.ingest, tm.model, tm.predictions, tm.residuals, tm.mosum, tm.breaks, tm.total]
+            out.write(f"{m}," + ",".join(f"{v:.6f}" for v in fields) + "\n")
+    return len(rows)

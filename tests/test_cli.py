@@ -50,9 +50,9 @@ def test_malformed_input_is_data_error(tmp_path, capsys):
     assert "magic" in capsys.readouterr().err
 
 
-def test_naive_backend_is_usage_error(tmp_path, capsys):
+def test_unknown_backend_is_usage_error(tmp_path, capsys):
     p = make_stack_file(tmp_path, m=5)
-    assert dispatch(["monitor", "--input", str(p), "--backend", "naive", "--out", str(tmp_path / "x")]) == 1
+    assert dispatch(["monitor", "--input", str(p), "--backend", "bogus", "--out", str(tmp_path / "x")]) == 1
 
 
 def test_unknown_flag_rejected(tmp_path, capsys):

@@ -135,12 +135,17 @@ class TestCriticalValueRequest:
 class TestMonitorConfig:
     @pytest.mark.parametrize("kw", [dict(harmonics=0), dict(freq=0.0), dict(history=8), dict(bandwidth=0),
                                     dict(bandwidth=101), dict(alpha=1.0), dict(crit_value=0.0),
-                                    dict(nan_mode="drop"), dict(backend="naive")])
+                                    dict(nan_mode="drop"), dict(backend="bogus")])
     def test_invalid(self, kw):
         args = dict(history=100, bandwidth=50, harmonics=3, freq=23.0)
         args.update(kw)
         with pytest.raises(ValueError):
             pkg.MonitorConfig(**args)
+
+    @pytest.mark.parametrize("backend", ["fused", "naive", "cuda"])
+    def test_backends_accepted(self, backend):
+        # the reference's two backends (engine.py:112,129-130) plus "cuda"; all run the GPU kernel
+        assert pkg.MonitorConfig(history=100, bandwidth=50, harmonics=3, freq=23.0, backend=backend).backend == backend
 
     def test_n_params(self):
         assert pkg.MonitorConfig(history=100, bandwidth=50, harmonics=3, freq=23.0).n_params == 8
@@ -179,3 +184,84 @@ class TestEngineContract:
         with pytest.raises(RuntimeError, match="CUDA|GPU"):
             pkg.monitor_batch(st, pkg.MonitorConfig(history=30, bandwidth=10, harmonics=1, freq=23.0,
                                                     crit_value=3.0))
+
+
+class TestReferenceSurface:
+    """Public names of the reference package (pkg/src/breakwatch/__init__.py:52-94)."""
+
+    # per-series CPU diagnostics of the reference that are not on the batch hot path
+    # (DESIGN.md §8): fit_history/predict/mosum_process/detect/amplitude_phase and their types
+    OUT_OF_SCOPE = {"HistoryModel", "MosumSeries", "amplitude_phase", "detect", "fit_history", "mosum_process",
+                    "predict"}
+    REFERENCE_ALL = {
+        "AllNanSeriesError", "BreakMap", "BreakResult", "BreakwatchError", "CriticalValueRequest", "CsvParseError",
+        "DegreesOfFreedomError", "DesignMatrix", "HistoryModel", "MappingMatrix", "MonitorConfig", "MosumSeries",
+        "PhaseTimings", "RankDeficiencyError", "SeriesStack", "StackCapacityError", "StackFormatError", "SynthSpec",
+        "TimeAxis", "ZeroResidualError", "amplitude_phase", "bench_scaling", "boundary_values",
+        "build_design_matrix", "critical_value", "detect", "fill_gaps", "fit_history", "fit_mapping", "generate",
+        "log_plus", "monitor_batch", "mosum_process", "predict", "profile_run", "read_series_csv", "read_stack",
+        "regular_axis", "resolve_crit_value", "resolve_threads", "write_bench_csv", "write_break_map",
+        "write_stack"}
+
+    def test_exports(self):
+        missing = self.REFERENCE_ALL - self.OUT_OF_SCOPE - set(pkg.__all__)
+        assert not missing, missing
+        for name in pkg.__all__:
+            assert hasattr(pkg, name), name
+
+    @pytest.mark.reference
+    def test_live_reference_names(self, reference):
+        assert set(reference.__all__) == self.REFERENCE_ALL
+
+    # fill KATs of the reference (test_engine.py:52-70)
+    @pytest.mark.parametrize("series, want", [
+        ([np.nan, 1.0, np.nan, 3.0], [1.0, 1.0, 1.0, 3.0]),
+        ([np.inf, 4.0, -np.inf], [4.0, 4.0, 4.0]),
+        ([1.0, 2.0, 3.0], [1.0, 2.0, 3.0]),
+        ([np.nan, np.nan, 5.0, np.nan], [5.0, 5.0, 5.0, 5.0]),
+    ])
+    def test_fill_gaps(self, series, want):
+        np.testing.assert_array_equal(pkg.fill_gaps(np.array(series)), np.array(want))
+
+    def test_fill_gaps_all_missing(self):
+        with pytest.raises(pkg.AllNanSeriesError):
+            pkg.fill_gaps(np.array([np.nan, np.inf]))
+
+    @pytest.mark.reference
+    def test_fill_gaps_matches_reference(self, reference):
+        ref_fill = reference.fill_gaps
+        rng = np.random.default_rng(5)
+        for _ in range(50):
+            v = rng.normal(size=30)
+            v[rng.random(30) < 0.4] = np.nan
+            if not np.isfinite(v).any():
+                continue
+            np.testing.assert_array_equal(pkg.fill_gaps(v), ref_fill(v))
+
+    def test_write_bench_csv(self, tmp_path):
+        import sys
+        from pathlib import Path
+
+        REFERENCE_SRC = Path("/root/reference/pkg/src")
+        rows = [(16, pkg.PhaseTimings(0.5, 0.25, 0.0, 0.0, 0.125, 0.0625, 0.9375))]
+        p = tmp_path / "b.csv"
+        assert pkg.write_bench_csv(rows, str(p)) == 1
+        assert p.read_text() == ("m,ingest,model,predictions,residuals,mosum,breaks,total\n"
+                                 "16,0.500000,0.250000,0.000000,0.000000,0.125000,0.062500,0.937500\n")
+        if not REFERENCE_SRC.exists():
+            return
+        if str(REFERENCE_SRC) not in sys.path:
+            sys.path.insert(0, str(REFERENCE_SRC))
+        from breakwatch.synth import write_bench_csv as ref_write
+
+        q = tmp_path / "r.csv"
+        ref_write(rows, str(q))
+        assert q.read_bytes() == p.read_bytes()
+
+    def test_bench_scaling_validation(self):
+        cfg = pkg.MonitorConfig(history=100, bandwidth=50, harmonics=3, freq=23.0, crit_value=3.0)
+        spec = pkg.SynthSpec(n_pixels=8, n_obs=200, freq=23.0)
+        with pytest.raises(ValueError):
+            pkg.bench_scaling([], cfg, spec)
+        with pytest.raises(ValueError):
+            pkg.bench_scaling([0], cfg, spec)
