@@ -74,8 +74,8 @@ def gather_maps(local: dict, rank: int, world: int, group=None) -> Optional[dict
 
 def gather_device_maps(valid, first_idx, max_abs, rank: int, world: int, group=None):
     """Whole-box result maps on rank 0 from the per-rank DEVICE maps (the kernel's raw u8 /
-    i32 / f32 outputs, 9 B per pixel), packed into one byte tensor per rank and gathered with
-    one collective over NVLink (NCCL; gloo with CPU tensors in the tests).  Returns
+    i32 / f32 outputs, 9 B per pixel), packed into one byte tensor per rank and gathered to
+    rank 0 with one collective over NVLink (NCCL; gloo with CPU tensors in the tests).  Returns
     (valid, first_idx, max_abs) tensors on rank 0 in global pixel order, None elsewhere."""
     import torch
     import torch.distributed as dist
@@ -91,8 +91,10 @@ def gather_device_maps(valid, first_idx, max_abs, rank: int, world: int, group=N
     width = 9 * max(sizes)
     buf = torch.zeros(width, dtype=torch.uint8, device=valid.device)
     buf[: packed.numel()] = packed
-    parts = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf, group=group)
+    # gather (not all_gather): only rank 0 receives, so each rank sends its maps once over
+    # NVLink instead of to every peer
+    parts = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+    dist.gather(buf, gather_list=parts, dst=0, group=group)
     if rank != 0:
         return None
     v, f, m = [], [], []

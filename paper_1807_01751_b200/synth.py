@@ -99,9 +99,55 @@ def _cloud_mask(rng, N: int, P: int, cols: int) -> np.ndarray:
     return mask
 
 
+def cloud_discs(n_obs: int, rows: int, cols: int, seed: int) -> list:
+    """Per-date cloud discs of a rows x cols scene, §8(d) C5: 0-5 discs per 512^2 area per
+    date (scaled to the scene), centres uniform over the scene, radius U(20, 150) px.  Drawn
+    from the SCENE seed on the host, so every rank's pixel band sees the same clouds.
+    Returns one float64 array [k, 3] (row, col, radius) per date."""
+    rng = np.random.default_rng(seed)
+    per = max(1.0, rows * cols / 512.0**2)
+    out = []
+    for _ in range(n_obs):
+        k = int(rng.integers(0, int(round(5 * per)) + 1))
+        out.append(np.stack([rng.uniform(0, rows, k), rng.uniform(0, cols, k), rng.uniform(20, 150, k)], axis=1))
+    return out
+
+
+def _apply_clouds(y, discs, cols: int, first_pixel: int):
+    """NaN every pixel of the band [first_pixel, first_pixel + P) of a row-major scene that lies
+    inside a disc of its date: each disc's 301x301 bounding box is tested on the device."""
+    import torch
+
+    dev = y.device
+    P = int(y.shape[1])
+    g0, g1 = first_pixel, first_pixel + P
+    r_lo, r_hi = g0 // cols, (g1 - 1) // cols
+    off = torch.arange(-150, 151, device=dev, dtype=torch.float64)
+    dr, dc = torch.meshgrid(off, off, indexing="ij")
+    dr, dc = dr.reshape(-1), dc.reshape(-1)
+    for d, disc in enumerate(discs):
+        keep = (disc[:, 0] + disc[:, 2] >= r_lo) & (disc[:, 0] - disc[:, 2] <= r_hi + 1)
+        disc = disc[keep]
+        for c0 in range(0, len(disc), 256):                     # bound the candidate tensor
+            q = torch.as_tensor(disc[c0:c0 + 256], device=dev)
+            rr = torch.floor(q[:, 0:1]) + dr[None, :]           # candidate pixel rows / cols
+            cc = torch.floor(q[:, 1:2]) + dc[None, :]
+            inside = ((rr - q[:, 0:1]) ** 2 + (cc - q[:, 1:2]) ** 2 <= q[:, 2:3] ** 2) & (cc >= 0) & (cc < cols)
+            gidx = (rr * cols + cc)[inside].long() - first_pixel
+            gidx = gidx[(gidx >= 0) & (gidx < P)]
+            y[d].index_fill_(0, gidx, float("nan"))
+    return y
+
+
 def device_stack(n_pixels: int, t: np.ndarray, freq: float, n_hist: int, nan_frac: float, seed: int,
-                 device="cuda", out=None, chunk: int = 1 << 22):
-    """float32 (N, P) NDVI-like stack generated directly in HBM (torch Philox)."""
+                 device="cuda", out=None, chunk: int = 1 << 22, clustered: bool = False,
+                 cols: Optional[int] = None, first_pixel: int = 0, scene_rows: Optional[int] = None,
+                 scene_seed: int = 20261022):
+    """float32 (N, P) NDVI-like stack generated directly in HBM (torch Philox).
+
+    clustered: missing values are the cloud discs of a scene_rows x cols scene (this stack is
+    the band [first_pixel, first_pixel + P) of it; the discs come from `scene_seed`, identical
+    on every rank) instead of i.i.d. Bernoulli(nan_frac) samples."""
     import torch
 
     N = t.size
@@ -121,10 +167,15 @@ def device_stack(n_pixels: int, t: np.ndarray, freq: float, n_hist: int, nan_fra
         start = torch.randint(n_hist, N, (w,), generator=g, device=dev)
         drop = -0.1 - 0.2 * torch.rand(w, generator=g, device=dev)
         blk += ((rows >= start[None, :]) & brk[None, :]) * drop[None, :]
-        blk[torch.rand((N, w), generator=g, device=dev) < nan_frac] = float("nan")
+        if not clustered:
+            blk[torch.rand((N, w), generator=g, device=dev) < nan_frac] = float("nan")
         dead = torch.rand(w, generator=g, device=dev) < 1e-4
         blk[:, dead] = float("nan")
         out[:, p0:p0 + w] = blk
+    if clustered:
+        cols = cols or int(np.sqrt(first_pixel + n_pixels))
+        scene_rows = scene_rows or (first_pixel + n_pixels + cols - 1) // cols
+        _apply_clouds(out, cloud_discs(N, scene_rows, cols, scene_seed), cols, first_pixel)
     return out
 
 
