@@ -103,11 +103,18 @@ int64_t smem_bytes_for(int N, int n, int h, int p, bool ring) {
 struct TmaRing {
     int mode, rows, cols;
 };
+// BWM_TMEM_COLS_MAX (power of two, 64..512): the largest TMEM ring a plan may allocate per CTA.
+// 512 = the whole SM's Tensor Memory: one CTA per SM, but the h = 250 ring of C4 fits on chip.
+int tmem_cols_max() {
+    const char* e = std::getenv("BWM_TMEM_COLS_MAX");
+    const int v = e ? std::atoi(e) : 256;
+    return v >= 512 ? 512 : v >= 256 ? 256 : v >= 128 ? 128 : 64;
+}
 TmaRing tma_ring_for(int h) {
     constexpr int R = bwm::kStageRows;
     const int L = ((h + R - 1) / R) * R;
     const int need = 2 * L;
-    if (h >= R && need <= 256) {
+    if (h >= R && need <= tmem_cols_max()) {
         int cols = 32;
         while (cols < need) cols *= 2;
         return {bwm::kRingTmem, L, cols};
