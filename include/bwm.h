@@ -214,6 +214,8 @@ typedef struct bwm_plan_info_t {
     int32_t const_bound;      /* boundary constant over the monitoring period (LEAN TMA variant)     */
     int32_t ctas_per_sm_tma_lean; /* persistent CTAs per SM, LEAN TMA variant                        */
     int32_t precise;          /* long horizon: float64 fitted values (LDG kernels); BWM_PRECISE=0/1   */
+    int32_t mma;              /* lagging-cursor geometry: fitted values on the tensor cores (BWM_MMA)  */
+    int64_t smem_mma;         /* dynamic shared memory per CTA of that kernel                         */
 } bwm_plan_info_t;
 
 int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info);

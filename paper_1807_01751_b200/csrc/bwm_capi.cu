@@ -32,6 +32,15 @@ BWM_DECLARE_PICK(12)
 BWM_DECLARE_PICK(14)
 BWM_DECLARE_PICK(16)
 BWM_DECLARE_PICK(18)
+#define BWM_DECLARE_PICK_MMA(NP) bwm::KernelFn bwm_pick_mma_p##NP(int lean);
+BWM_DECLARE_PICK_MMA(4)
+BWM_DECLARE_PICK_MMA(6)
+BWM_DECLARE_PICK_MMA(8)
+BWM_DECLARE_PICK_MMA(10)
+BWM_DECLARE_PICK_MMA(12)
+BWM_DECLARE_PICK_MMA(14)
+BWM_DECLARE_PICK_MMA(16)
+BWM_DECLARE_PICK_MMA(18)
 #define BWM_DECLARE_PICK_MASKED(NP) bwm::KernelFn bwm_pick_masked_p##NP(int big, int keep);
 BWM_DECLARE_PICK_MASKED(4)
 BWM_DECLARE_PICK_MASKED(6)
@@ -113,7 +122,7 @@ int tmem_cols_max() {
 TmaRing tma_ring_for(int h) {
     constexpr int R = bwm::kStageRows;
     const int L = ((h + R - 1) / R) * R;
-    const int need = 2 * L;
+    const int need = 2 * (L + (bwm::kMirror ? R : 0));   // 2 columns per ring row; mirror rows L..L+R-1
     if (h >= R && need <= tmem_cols_max()) {
         int cols = 32;
         while (cols < need) cols *= 2;
@@ -150,12 +159,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D map of a time-major float32 block: dim0 = pixels (contiguous), dim1 = dates (stride ld)
-int encode_map(CUtensorMap* map, const float* y, int64_t n_pixels, int n_obs, int64_t ld) {
+int encode_map(CUtensorMap* map, const float* y, int64_t n_pixels, int n_obs, int64_t ld, int box_px = bwm::kWarpPx) {
     auto fn = encode_fn();
     if (!fn) return set_err((int)cudaErrorNotSupported, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[2] = {(cuuint64_t)n_pixels, (cuuint64_t)n_obs};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)bwm::kWarpPx, (cuuint32_t)bwm::kStageRows};
+    const cuuint32_t box[2] = {(cuuint32_t)box_px, (cuuint32_t)bwm::kStageRows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(y), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -208,6 +217,20 @@ KernelFn pick_masked(int p, bool big, bool keep) {
         case 14: return bwm_pick_masked_p14(big, keep);
         case 16: return bwm_pick_masked_p16(big, keep);
         case 18: return bwm_pick_masked_p18(big, keep);
+        default: return nullptr;
+    }
+}
+
+KernelFn pick_mma(int p, bool lean) {
+    switch (p) {
+        case 4: return bwm_pick_mma_p4(lean);
+        case 6: return bwm_pick_mma_p6(lean);
+        case 8: return bwm_pick_mma_p8(lean);
+        case 10: return bwm_pick_mma_p10(lean);
+        case 12: return bwm_pick_mma_p12(lean);
+        case 14: return bwm_pick_mma_p14(lean);
+        case 16: return bwm_pick_mma_p16(lean);
+        case 18: return bwm_pick_mma_p18(lean);
         default: return nullptr;
     }
 }
@@ -280,6 +303,11 @@ struct bwm_plan {
     mutable unsigned int* d_fix_count = nullptr;
     mutable int64_t fix_cap = 0;
     int bpm_tma_lean = 0;              // resident CTAs per SM of the LEAN TMA variant
+    // lagging-cursor geometries: fitted values on the tensor cores (bwm_kernel_mma.cuh)
+    bool use_mma = false;
+    int64_t smem_mma = 0;
+    float* d_zb_cur = nullptr;
+    float* d_zb_lag = nullptr;
     // masked-NaN mode (bwm_kernel_masked.cuh)
     bool masked = false;
     bool mbig = false;                 // x x^T table + rings in global memory
@@ -322,6 +350,8 @@ static void plan_free_tables(bwm_plan* plan) {
     cudaFree(plan->d_xx);
     cudaFree(plan->d_gfull);
     cudaFree(plan->d_ring);
+    cudaFree(plan->d_zb_cur);
+    cudaFree(plan->d_zb_lag);
     if (plan->scratch_ev) cudaEventDestroy(plan->scratch_ev);
     plan->scratch_ev = nullptr;
 }
@@ -652,6 +682,51 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
             return fail(e, "cudaMemcpy");
     }
 
+    // Lagging-cursor geometries (large h): the tensor-core fitted-value kernel (bwm_kernel_mma.cuh)
+    // when BWM_MMA=1 and its tables fit shared memory.  Opt-in: measured SLOWER than the FFMA
+    // kernel at C4 (10.2 vs 8.2 ms; profiles/r02_C4_mma_ncu_summary.txt), so not the default.
+    if (plan->smem_tma > 0 && (plan->tring.mode == (int)bwm::kRingLag || plan->tring.mode == (int)bwm::kRingLagT)) {
+        const char* mma_env = getenv("BWM_MMA");
+        const bool want = mma_env && std::strcmp(mma_env, "1") == 0;
+        const int64_t sm = bwm::mma_smem_bytes(N, n, h, p);
+        if (want && sm <= max_optin && plan->d_xtd) {
+            const bwm::MmaGeom g = bwm::mma_geom(N, n, h);
+            const int KS = bwm::mma_ks(p);
+            // [split][K-step][group][K chunk][8 rows][4]: z_t split into tf32 hi + lo
+            auto build = [&](int date0, int groups, std::vector<float>& tab) {
+                tab.assign((size_t)2 * KS * groups * 64, 0.f);
+                for (int gi = 0; gi < groups; ++gi)
+                    for (int r = 0; r < 8; ++r) {
+                        const int t = date0 + 8 * gi + r;
+                        if (t < 0 || t >= N) continue;
+                        for (int k = 0; k < p; ++k) {
+                            const float v = (float)xtd[(size_t)t * sp + k];
+                            const float hi = tf32_round(v), lo = tf32_round(v - hi);
+                            const int ks = k / 8, kc = (k % 8) / 4, e = k % 4;
+                            const size_t in = (size_t)gi * 64 + kc * 32 + r * 4 + e;
+                            tab[((size_t)(0 * KS + ks) * groups) * 64 + in] = hi;
+                            tab[((size_t)(1 * KS + ks) * groups) * 64 + in] = lo;
+                        }
+                    }
+            };
+            std::vector<float> tc, tl;
+            build(g.w0, g.gcur, tc);
+            build(g.t3 - h, g.glag, tl);
+            if ((e = cudaMalloc(&plan->d_zb_cur, tc.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+            if ((e = cudaMalloc(&plan->d_zb_lag, tl.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+            if ((e = cudaMemcpy(plan->d_zb_cur, tc.data(), tc.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+                return fail(e, "cudaMemcpy");
+            if ((e = cudaMemcpy(plan->d_zb_lag, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+                return fail(e, "cudaMemcpy");
+            for (int lean = 0; lean < 2; ++lean)
+                if ((e = cudaFuncSetAttribute((const void*)pick_mma(p, lean), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              max_optin)) != cudaSuccess)
+                    return fail(e, "cudaFuncSetAttribute");
+            plan->use_mma = true;
+            plan->smem_mma = sm;
+        }
+    }
+
     // LEAN TMA variant: the boundary is one value over the whole monitoring period
     plan->const_bound = true;
     for (int j = 1; j < N - n; ++j) plan->const_bound = plan->const_bound && bd[(size_t)j] == bd[0];
@@ -862,6 +937,20 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         kp.mosum = out->mosum ? out->mosum + p0 : nullptr;
         kp.sup = out->sup_stat ? out->sup_stat + p0 : nullptr;
         const bool lean = kind == kTma && plan->const_bound && !out->mosum && !out->mo_mean;
+        if (kind == kTma && plan->use_mma) {
+            // fitted values on the tensor cores: 1 CTA of two 4-warp sets per SM
+            int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y);
+            if (rc) return rc;
+            kp.zb_cur = plan->d_zb_cur;
+            kp.zb_lag = plan->d_zb_lag;
+            const int64_t tiles = cnt / bwm::kTile;
+            const int64_t grid = std::min<int64_t>((tiles + bwm::kMmaSets - 1) / bwm::kMmaSets, (int64_t)plan->sms);
+            pick_mma(d.n_params, lean)<<<(unsigned)grid, bwm::kMmaThreads, (size_t)plan->smem_mma, st>>>(kp);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
+            ++launched;
+            continue;
+        }
         KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode | (lean ? bwm::kTmaLean : 0)
                                                           : (plan->ring ? 0 : (int)bwm::kRingLag));
         const int64_t tiles = (cnt + bwm::kTile - 1) / bwm::kTile;
@@ -871,6 +960,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         if (kind == kTma) {
             int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y);
             if (rc) return rc;
+            if ((rc = encode_map(&kp.tmap_pf, kp.y, cnt, d.n_obs, ld_y, bwm::kTile))) return rc;
         }
         fn<<<(unsigned)grid, threads_of(kind), sm, st>>>(kp);
         cudaError_t e = cudaGetLastError();
@@ -1321,6 +1411,8 @@ int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {
     info->const_bound = plan->const_bound ? 1 : 0;
     info->ctas_per_sm_tma_lean = plan->bpm_tma_lean;
     info->precise = plan->precise ? 1 : 0;
+    info->mma = plan->use_mma ? 1 : 0;
+    info->smem_mma = plan->smem_mma;
     return BWM_OK;
 }
 

@@ -25,6 +25,7 @@ constexpr int kComp = BWM_COMP;       // dates per 2Sum-compensated block partia
 
 struct KParams {
     CUtensorMap tmap;           // TMA kernel: 2-D map of y (pixels x dates), box 64 px x 8 dates
+    CUtensorMap tmap_pf;        // the same stack, box 256 px x 8 dates: the CTA-wide L2 prefetch
     const float* y;             // this launch's pixel 0, row stride ld_y (elements)
     int64_t ld_y;
     int64_t n_pixels;
@@ -64,6 +65,9 @@ struct KParams {
     unsigned int fix_cap;       // list capacity; pixels past it keep their float32 result
     float fix_ratio;
     int64_t fix_base;
+    // tensor-core fitted values (bwm_kernel_mma.cuh): Z^T split into tf32 hi/lo B tables
+    const float* zb_cur;        // current dates [w0, ...)
+    const float* zb_lag;        // lag dates [t3 - h, ...)
 };
 
 // append pixel `px` (launch-relative) to the fixup list when its history fit is ill-conditioned:

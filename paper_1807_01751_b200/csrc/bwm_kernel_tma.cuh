@@ -25,9 +25,10 @@
 // MOSUM residual ring (r_{t-h} for the add-one/drop-one recurrence, _kernels.py:31-34):
 //   MODE kRingTmem : in Tensor Memory.  Each thread owns its TMEM lane; ring row q of the
 //                    pixel pair occupies columns 2q, 2q+1; L = ring rows (multiple of the
-//                    stage height R, >= h), 2L columns (64 at h <= 32, so TMEM admits 8 CTAs
-//                    per SM).  Per stage: R/8 tcgen05.st.x16, and R/8 tcgen05.ld.x16 for the
-//                    lagged rows (R .x2 loads on the stages whose window wraps).
+//                    stage height R, >= h), plus R MIRROR rows L..L+R-1 that duplicate rows
+//                    0..R-1 (every write of a row < R also writes row q + L), so the R lagged
+//                    rows of a stage are always one contiguous run: R/8 tcgen05.st.x16 and R/8
+//                    tcgen05.ld.x16 per stage, no wrap path.  2(L+R) columns: 128 at h <= 56.
 //   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged date t-h (large h); tables
 //                    read through L1 (any series length).  kRingLagT: the same with the tables
 //                    staged in shared memory (when they fit).
@@ -58,6 +59,22 @@ constexpr int kStageRows = BWM_STAGE_ROWS;      // dates per stage (multiple of 
 #define BWM_STAGES_LAG 3
 #endif
 constexpr int kStages = BWM_STAGES;             // stage ring depth per warp (TMEM-ring mode)
+#ifndef BWM_RING_MIRROR
+#define BWM_RING_MIRROR 1  // TMEM ring with R mirror rows (no wrapped lag loads)
+#endif
+#ifndef BWM_LAZY_CROSS
+#define BWM_LAZY_CROSS 1   // LEAN: first-crossing search once per stage from the running max
+#endif
+constexpr bool kMirror = BWM_RING_MIRROR != 0;
+#ifndef BWM_PF_AHEAD
+#define BWM_PF_AHEAD 0     // CTA-wide L2 prefetch this many stages ahead of a warp's TMA issue (0: off;
+#endif                     // measured 2.2x SLOWER at C2 with 4 stages, every warp)
+#ifndef BWM_SYNC_EVERY
+#define BWM_SYNC_EVERY 0   // named CTA barrier every this many stages (power of 2; 0: free-running warps)
+#endif
+#ifndef BWM_PF_ALL
+#define BWM_PF_ALL 1       // every warp prefetches (robust to warp drift); 0: warp 0 only
+#endif
 // the lagging-cursor mode moves two boxes per stage (dates t and t-h): 3 stages = 6 boxes
 // (kRingLag: tables in global memory, 3 stages, 3 CTAs/SM; kRingLagT: tables in smem, 2 stages,
 //  2 CTAs/SM — measured 8.85 vs 8.11 ms at C4, so kRingLagT whenever its tables fit)
@@ -137,6 +154,19 @@ __device__ __forceinline__ void tma_box2_elect(uint32_t dst, const CUtensorMap* 
         "}" ::"r"(dst),
         "r"(dst + (uint32_t)(kStageRows * kWarpPx * 4)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
         "r"(bar), "r"(bytes), "r"(y2)
+        : "memory");
+}
+
+// L2 prefetch of a (256 px, R dates) box of the CTA's tile: DRAM sees the tile's 1 KB row
+// segments together even when the four warps' own 64-px boxes are issued at different times
+// (free-running 64-px boxes stream at 3.6 TB/s, 256-px boxes at 7.2 TB/s:
+// profiles/probe/tma_probe_r01.txt); the per-warp TMA loads that follow hit L2.
+__device__ __forceinline__ void tma_prefetch_elect(const CUtensorMap* map, int x, int y) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n\t"
+        "}" ::"l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y)
         : "memory");
 }
 
@@ -275,7 +305,24 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
     int64_t itile = blockIdx.x;
     int istage = 0;
     int xw = (int)(itile * kTile) + wu * kWarpPx;           // x of the cursor's tile slice
+    // L2 prefetch cursor: BWM_PF_AHEAD stages ahead of the issue cursor
+    constexpr int PF = BWM_PF_AHEAD;
+    const bool pf_warp = PF > 0 && (BWM_PF_ALL || wu == 0);
+    int64_t ptile = blockIdx.x;
+    int pstage = 0;
+    auto prefetch_next = [&]() {
+        if (ptile < n_tiles) {
+            const int r0 = s_rows[pstage];
+            tma_prefetch_elect(&prm.tmap_pf, (int)(ptile * kTile), r0);
+            if (kLag && pstage >= st1 + st2 && r0 >= h) tma_prefetch_elect(&prm.tmap_pf, (int)(ptile * kTile), r0 - h);
+        }
+        if (++pstage == tile_stages) {
+            pstage = 0;
+            ptile += gridDim.x;
+        }
+    };
     auto issue_into = [&](int slot) {
+        if (pf_warp) prefetch_next();
         if (itile >= n_tiles) return;
         const int r0 = s_rows[istage];
         const uint32_t dst = stage_u32 + (uint32_t)(slot * SB), bar = bar_u32 + (uint32_t)(slot * 8);
@@ -290,6 +337,10 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         }
     };
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap)) : "memory");
+    if (pf_warp) {
+        if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap_pf)) : "memory");
+        for (int s = 0; s < PF; ++s) prefetch_next();       // then one per issue, PF stages ahead
+    }
     for (int s = 0; s < S; ++s) issue_into(s);
 
     const int L = prm.ring_rows;
@@ -300,7 +351,10 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
     const int q_w0 = MODE == kRingTmem ? w0 % L : 0, q_wstart = MODE == kRingTmem ? wstart % L : 0;
     const int q_t3 = MODE == kRingTmem ? t3 % L : 0, q_t3h = MODE == kRingTmem ? ((t3 - h) % L + L) % L : 0;
     const int q_nh = MODE == kRingTmem ? (n - h) % L : 0;
-    auto ring_put_row = [&](int q, float2 v) { tmem_st2(tcol(q), v); };   // q < L
+    auto ring_put_row = [&](int q, float2 v) {                             // q < L (+ mirror)
+        tmem_st2(tcol(q), v);
+        if (kMirror && q < R) tmem_st2(tcol(q + L), v);
+    };
     auto ring_ld2 = [&](int q, float2& v) {                                // no wait
         uint32_t a, b;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(tcol(q)) : "memory");
@@ -312,15 +366,15 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         tmem_wait_ld();
         return v;
     };
-    // R consecutive ring rows starting at row q0 < L: R/8 tcgen05.ld.x16 when they do not wrap,
-    // else one .x2 per row (warp-uniform branch; with L = 32, one stage in four wraps)
+    // R consecutive ring rows starting at row q0 < L: rows past L are the mirror rows, so the
+    // run never wraps — R/8 tcgen05.ld.x16
     auto ring_load = [&](int q0, float2 (&v)[R]) {
         tmem_wait_st();
-        if (q0 + R <= L) {
+        if (kMirror || q0 + R <= L) {
 #pragma unroll
             for (int c8 = 0; c8 < R / 8; ++c8)
                 tmem_ld16(tcol(q0 + 8 * c8), *reinterpret_cast<float2(*)[8]>(&v[8 * c8]));
-        } else {
+        } else {                                             // no mirror: the run wraps
 #pragma unroll
             for (int k = 0; k < R; ++k) ring_ld2(q0 + k >= L ? q0 + k - L : q0 + k, v[k]);
             tmem_wait_ld();
@@ -330,6 +384,11 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
 #pragma unroll
         for (int c8 = 0; c8 < R / 8; ++c8)
             tmem_st16(tcol(q0 + 8 * c8), *reinterpret_cast<const float2(*)[8]>(&v[8 * c8]));
+        if (kMirror && q0 == 0) {                            // rows 0..R-1: their mirror too
+#pragma unroll
+            for (int c8 = 0; c8 < R / 8; ++c8)
+                tmem_st16(tcol(L + 8 * c8), *reinterpret_cast<const float2(*)[8]>(&v[8 * c8]));
+        }
     };
     int cur = 0;
     uint32_t ph = 0;
@@ -342,7 +401,10 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         next_ready = mbar_test(full + nc, nc == 0 ? ph ^ 1 : ph);
         return reinterpret_cast<const float2*>(my_stage + cur * SB) + lane;
     };
+    uint32_t n_rel = 0;
     auto release = [&]() {
+        if (BWM_SYNC_EVERY > 0 && ((++n_rel) & (BWM_SYNC_EVERY - 1)) == 0)
+            asm volatile("bar.sync 1, %0;" ::"n"(kTmaThreads) : "memory");   // keep the 4 warps' boxes coherent
         __syncwarp();
         issue_into(cur);                             // re-arm this slot kStages ahead
         if (++cur == S) { cur = 0; ph ^= 1; }
@@ -530,6 +592,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
                 for (int q = 0; q < R / 4; ++q)
                     b4[q] = LEAN ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(s_bd + t0)[q];
                 const float* xrow = s_xt + t0 * SP;
+                float2 acck[R];                          // LEAN: window sums of the stage
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const int t = t0 + k;
@@ -541,8 +604,31 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
                     } else {
                         old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), xrow + (k - h) * SP, nb);
                     }
-                    const float4 bq4 = b4[k >> 2];
-                    step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
+                    if (LEAN && BWM_LAZY_CROSS) {
+                        // constant boundary: the first crossing is the first date whose running max
+                        // exceeds it, so the per-date test moves out of the loop (below)
+                        acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
+                        acck[k] = acc;
+                        mx.x = fmaxf(mx.x, fabsf(acc.x));
+                        mx.y = fmaxf(mx.y, fabsf(acc.y));
+                    } else {
+                        const float4 bq4 = b4[k >> 2];
+                        step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
+                    }
+                }
+                if (LEAN && BWM_LAZY_CROSS) {
+                    // strict crossing (_kernels.py:47) of the stage's first date past the boundary;
+                    // taken at most once per pixel
+                    if (first0 == 0x7fffffff && mx.x > bsc.x) {
+#pragma unroll
+                        for (int k = R - 1; k >= 0; --k)
+                            if (fabsf(acck[k].x) > bsc.x) first0 = t0 + k - n + 1;
+                    }
+                    if (first1 == 0x7fffffff && mx.y > bsc.y) {
+#pragma unroll
+                        for (int k = R - 1; k >= 0; --k)
+                            if (fabsf(acck[k].y) > bsc.y) first1 = t0 + k - n + 1;
+                    }
                 }
                 if (MODE == kRingTmem) ring_store(wb, newv);
             } else {

@@ -3,6 +3,7 @@
 #include "bwm_kernel_ldg.cuh"
 #include "bwm_kernel_tma.cuh"
 #include "bwm_kernel_masked.cuh"
+#include "bwm_kernel_mma.cuh"
 
 namespace bwm {
 enum Kind { kLdgFast = 0, kLdgSafe = 1, kTma = 2 };
@@ -31,6 +32,13 @@ constexpr int kTmaLean = 0x10;   // pick(): OR into the TMA ring mode for the LE
                        : (mode & 0xF) == bwm::kRingLagT ? bwm::monitor_kernel_tma<NP, bwm::kRingLagT, false>     \
                                                        : bwm::monitor_kernel_tma<NP, bwm::kRingLag, false>;      \
         }                                                                                        \
+    }
+
+// Defines bwm::KernelFn bwm_pick_mma_p<NP>(int lean): the lagging-cursor kernel with the
+// fitted values on the tensor cores (bwm_kernel_mma.cuh).
+#define BWM_DEFINE_PICK_MMA(NP)                                                                  \
+    bwm::KernelFn bwm_pick_mma_p##NP(int lean) {                                                 \
+        return lean ? bwm::monitor_kernel_mma<NP, true> : bwm::monitor_kernel_mma<NP, false>;   \
     }
 
 // Defines bwm::KernelFn bwm_pick_masked_p<NP>(int big, int keep): the masked-NaN kernel with

@@ -3,3 +3,4 @@
 
 BWM_DEFINE_PICK(10)
 BWM_DEFINE_PICK_MASKED(10)
+BWM_DEFINE_PICK_MMA(10)

@@ -3,3 +3,4 @@
 
 BWM_DEFINE_PICK(12)
 BWM_DEFINE_PICK_MASKED(12)
+BWM_DEFINE_PICK_MMA(12)

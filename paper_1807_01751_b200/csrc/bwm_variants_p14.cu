@@ -3,3 +3,4 @@
 
 BWM_DEFINE_PICK(14)
 BWM_DEFINE_PICK_MASKED(14)
+BWM_DEFINE_PICK_MMA(14)

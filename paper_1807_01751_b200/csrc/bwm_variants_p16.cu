@@ -3,3 +3,4 @@
 
 BWM_DEFINE_PICK(16)
 BWM_DEFINE_PICK_MASKED(16)
+BWM_DEFINE_PICK_MMA(16)

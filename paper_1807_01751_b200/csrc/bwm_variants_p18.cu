@@ -3,3 +3,4 @@
 
 BWM_DEFINE_PICK(18)
 BWM_DEFINE_PICK_MASKED(18)
+BWM_DEFINE_PICK_MMA(18)

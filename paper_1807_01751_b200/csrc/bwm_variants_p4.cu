@@ -3,3 +3,4 @@
 
 BWM_DEFINE_PICK(4)
 BWM_DEFINE_PICK_MASKED(4)
+BWM_DEFINE_PICK_MMA(4)

@@ -3,3 +3,4 @@
 
 BWM_DEFINE_PICK(6)
 BWM_DEFINE_PICK_MASKED(6)
+BWM_DEFINE_PICK_MMA(6)

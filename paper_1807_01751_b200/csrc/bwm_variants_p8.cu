@@ -3,3 +3,4 @@
 
 BWM_DEFINE_PICK(8)
 BWM_DEFINE_PICK_MASKED(8)
+BWM_DEFINE_PICK_MMA(8)

@@ -268,3 +268,32 @@ def test_long_series(N, n, h, k):
     border = bo.borderline_from_pairs(pairs, N - n, y.shape[1], ref.first_idx, first_gpu)
     assert not np.any((first_gpu != ref.first_idx) & ~border & ref.valid)
     np.testing.assert_allclose(bm.max_abs_mo[ref.valid], ref.max_abs_mo[ref.valid], rtol=RTOL, atol=0)
+
+
+@pytest.mark.parametrize("name", ["c4_tile", "c5_tile"])
+def test_tensor_core_fitted_values(name, monkeypatch):
+    """The opt-in lagging-cursor kernel with its fitted values on the tensor cores
+    (BWM_MMA=1, bwm_kernel_mma.cuh: 3xTF32 tcgen05.mma) meets the same parity bar as the FFMA
+    kernels: a different arithmetic for z_t^T beta_Q, so the check is the oracle tolerance, not
+    bit identity.  c5_tile (h = 50) is forced onto the lagging cursor with a 64-column TMEM cap."""
+    import torch
+
+    from paper_1807_01751_b200.device import DevicePlan
+    from paper_1807_01751_b200.model import TimeAxis
+
+    case = load(name)
+    monkeypatch.setenv("BWM_MMA", "1")
+    monkeypatch.setenv("BWM_TMEM_COLS_MAX", "64")
+    plan = DevicePlan(TimeAxis(case.t), case.freq, case.k, case.n, case.h, case.crit, "cuda")
+    monkeypatch.delenv("BWM_MMA")
+    monkeypatch.delenv("BWM_TMEM_COLS_MAX")
+    assert plan.info()["mma"] == 1
+    n = case.n
+    y = torch.as_tensor(case.y, device="cuda")
+    for kw in (dict(), dict(mean=True, keep_mosum=True)):         # LEAN and general variants
+        res = plan.run_device(y, **kw)
+        fi = res.first_idx.cpu().numpy()
+        check_parity(case, np.where(fi > 0, fi + n, 0), res.max_abs.cpu().numpy().astype(np.float64),
+                     res.valid.cpu().numpy().astype(bool),
+                     None if res.mo_mean is None else res.mo_mean.cpu().numpy(),
+                     None, None if res.mosum is None else res.mosum.cpu().numpy())
