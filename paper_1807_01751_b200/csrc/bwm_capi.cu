@@ -139,9 +139,9 @@ int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
     // Z^T (rows < n double as Q^T; global memory in the lagging-cursor mode) + bound
     int64_t fl = (mode == bwm::kRingLag ? 0 : (int64_t)N * sp) + ((N + 3) & ~3);
     const int S = bwm::stages_for(mode);
-    int64_t bytes = bwm::kWarps * S * bwm::tma_stage_bytes(mode) + fl * 4;
+    int64_t bytes = bwm::tma_stage_region(mode, S) + fl * 4;
     const int sched = 2 * ((N + bwm::kStageRows - 1) / bwm::kStageRows) + 4;   // stage schedule table
-    return bytes + bwm::kWarps * S * 8 + 16 + 4 * sched;  // + per-warp stage barriers, TMEM slot
+    return bytes + bwm::tma_barriers(mode, S) * 8 + (BWM_SHARED_BOX ? 4 * S : 0) + 16 + 4 * sched;  // + stage barriers, tickets, TMEM slot
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed).
@@ -238,7 +238,7 @@ KernelFn pick_mma(int p, bool lean) {
 // masked kernel: x x^T table and rings in shared memory up to this size, else global (BIG)
 constexpr int64_t kMaskedSmemMax = 96 << 10;
 
-int threads_of(Kind k) { return k == kTma ? bwm::kTmaThreads : bwm::kThreads; }
+int threads_of(Kind k, int tma_mode = bwm::kRingTmem) { return k == kTma ? bwm::tma_threads(tma_mode) : bwm::kThreads; }
 
 }  // namespace
 
@@ -515,7 +515,7 @@ int64_t bwm_smem_bytes(const bwm_dims* d) {
     int tmode = mode;
     if (tma > kOptin && mode == (int)bwm::kRingTmem) tmode = bwm::kRingLag;
     if (tmode == (int)bwm::kRingLag &&
-        smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, bwm::kRingLagT) <= (110 << 10))
+        smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, bwm::kRingLagT) <= (BWM_LAGT_WARPS > 4 ? kOptin : (110 << 10)))
         tmode = bwm::kRingLagT;
     if (tmode != mode) tma = smem_bytes_tma(d->n_obs, d->n_hist, d->bandwidth, d->n_params, tmode);
     return tma > 0 ? tma : ldg;
@@ -559,7 +559,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         }
         // lagging cursor: tables staged in smem when they fit (kRingLagT), else through L1
         if (plan->tring.mode == (int)bwm::kRingLag &&
-            smem_bytes_tma(N, n, h, p, bwm::kRingLagT) <= std::min<int64_t>(optin, 110 << 10)) {
+            smem_bytes_tma(N, n, h, p, bwm::kRingLagT) <= std::min<int64_t>(optin, BWM_LAGT_WARPS > 4 ? optin : (110 << 10))) {
             plan->tring = {(int)bwm::kRingLagT, 0, 0};
             plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->tring.mode);
         }
@@ -738,7 +738,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         cudaError_t err = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
         if (err != cudaSuccess) return err;
         int nb = 0;
-        if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, threads_of(kind), (size_t)sm)) !=
+        if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, threads_of(kind, plan->tring.mode), (size_t)sm)) !=
             cudaSuccess)
             return err;
         if (kind == kTma && plan->tring.mode == bwm::kRingTmem) {
@@ -746,7 +746,7 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
             // TMEM (reports 1).  Allocation is dynamic (tcgen05.alloc + relinquish_alloc_permit),
             // so residency is bounded by registers, shared memory, threads and our own column
             // budget: 512 columns per SM / tmem_cols per CTA.
-            nb = resident_ctas((const void*)fn, threads_of(kind), sm, plan->tring.cols, device, &err);
+            nb = resident_ctas((const void*)fn, threads_of(kind, plan->tring.mode), sm, plan->tring.cols, device, &err);
             if (err != cudaSuccess) return err;
         }
         *nb_out = nb;
@@ -895,7 +895,9 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
                         (ld_y % 4 == 0) && out_al;
     const bool ldg_ok = al(y, 8) && (ld_y % 2 == 0);
     const Kind main_kind = tma_ok ? kTma : kLdgFast;
-    const int64_t full = (tma_ok || ldg_ok) ? (n_pixels / bwm::kTile) * bwm::kTile : 0;
+    // whole tiles of the main kernel (the TMA kernel's tile is 64 px per warp of its CTA)
+    const int64_t main_tile = main_kind == kTma && !plan->use_mma ? bwm::tma_tile(plan->tring.mode) : bwm::kTile;
+    const int64_t full = (tma_ok || ldg_ok) ? (n_pixels / main_tile) * main_tile : 0;
     if (fixup) {
         // capacity: every pixel of small calls, 4M entries (32 MB) at most — flagged pixels are
         // rare on real data, and a near-capacity stack must not run out of HBM for the list
@@ -953,16 +955,16 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         }
         KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode | (lean ? bwm::kTmaLean : 0)
                                                           : (plan->ring ? 0 : (int)bwm::kRingLag));
-        const int64_t tiles = (cnt + bwm::kTile - 1) / bwm::kTile;
+        const int64_t tile = kind == kTma ? bwm::tma_tile(plan->tring.mode) : bwm::kTile;
+        const int64_t tiles = (cnt + tile - 1) / tile;
         const int bpm = lean ? plan->bpm_tma_lean : plan->blocks_per_sm[kind];
         const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * bpm);
         const size_t sm = (size_t)(kind == kTma ? plan->smem_tma : plan->smem);
         if (kind == kTma) {
-            int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y);
+            int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y, BWM_SHARED_BOX ? (int)tile : bwm::kWarpPx);
             if (rc) return rc;
-            if ((rc = encode_map(&kp.tmap_pf, kp.y, cnt, d.n_obs, ld_y, bwm::kTile))) return rc;
         }
-        fn<<<(unsigned)grid, threads_of(kind), sm, st>>>(kp);
+        fn<<<(unsigned)grid, threads_of(kind, plan->tring.mode), sm, st>>>(kp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
         ++launched;

@@ -25,7 +25,6 @@ constexpr int kComp = BWM_COMP;       // dates per 2Sum-compensated block partia
 
 struct KParams {
     CUtensorMap tmap;           // TMA kernel: 2-D map of y (pixels x dates), box 64 px x 8 dates
-    CUtensorMap tmap_pf;        // the same stack, box 256 px x 8 dates: the CTA-wide L2 prefetch
     const float* y;             // this launch's pixel 0, row stride ld_y (elements)
     int64_t ld_y;
     int64_t n_pixels;

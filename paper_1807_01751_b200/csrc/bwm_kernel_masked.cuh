@@ -110,7 +110,7 @@ __host__ __device__ inline int64_t masked_smem_bytes(int N, int n, int h, int p,
     int64_t bytes = big ? 0 : (((int64_t)(N + kMaskD) * sp * 4 + 127) / 128) * 128;
     bytes += (int64_t)kMaskBStages * gram_nn(p) * 128;                      // x x^T tile ring
     if (!big) bytes += (int64_t)masked_scratch_words(h, p) * kMaskThreads * 4;
-    return bytes + (2 * kMaskBStages + kMaskABufs) * 8 + 16;                // mbarriers + TMEM slot
+    return bytes + (2 * kMaskBStages + kMaskABufs) * 8 + 32;                // mbarriers + TMEM slot + tickets
 }
 
 // Column J of an in-place float32 Cholesky factorisation of the packed lower triangle L,
@@ -140,6 +140,11 @@ __device__ __forceinline__ void chol_col(float (&L)[NP * (NP + 1) / 2], float (&
 // idle lanes of a tail tile read this NaN (stride 0): every date missing, no per-row test
 static __device__ const unsigned int kNanRow[1] = {0x7fc00000u};
 
+#ifndef BWM_MASK_TICKET
+#define BWM_MASK_TICKET 0   // 1: the last warp to stage a block's mask rows issues its MMAs instead of a
+                            // __syncthreads (measured 5% SLOWER at C2 and C5: the barrier keeps the
+                            // four warps' scalar row loads coherent)
+#endif
 #ifndef BWM_MASK_MINB
 #define BWM_MASK_MINB 4
 #endif
@@ -166,11 +171,13 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
     uint64_t* b_empty = s_bar + S;         // [S]  MMAs reading the tile are done
     uint64_t* m_done = s_bar + 2 * S;      // [AB] MMAs reading A buffer b are done
     uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 2 * S + AB);
+    uint32_t* s_tick = s_tmem + 1;                // [AB] mask-row tickets (BWM_MASK_TICKET)
     const int tid = threadIdx.x, warp = tid >> 5;
     if (!BIG)
         for (int i = tid; i < (N + D) * SP; i += kMaskThreads) s_xs[i] = i < N * SP ? prm.xt[i] : 0.f;
     if (tid == 0) {
         for (int i = 0; i < 2 * S + AB; ++i) mbar_init(s_bar + i, 1);
+        for (int i = 0; i < AB; ++i) s_tick[i] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     constexpr uint32_t kCols = (uint32_t)masked_tmem_cols(NP);
@@ -272,8 +279,19 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
             tmem_st16(a_col + lane_off + 16 * ab, wv);
             tmem_wait_st();
             tmem_fence_before();
-            __syncthreads();
-            if (tid == 0) {
+            bool issuer;
+            if (BWM_MASK_TICKET) {
+                // the last of the four warps to stage its rows of this block issues the MMAs
+                __syncwarp();
+                uint32_t t = 0;
+                if ((tid & 31) == 0)
+                    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(t) : "r"(smem_u32(s_tick + ab)) : "memory");
+                issuer = (__shfl_sync(0xffffffffu, t, 0) & 3u) == 3u && (tid & 31) == 0;
+            } else {
+                __syncthreads();
+                issuer = tid == 0;
+            }
+            if (issuer) {
                 tmem_fence_after();
                 const int st = (int)(q % S);
                 mbar_wait(b_full + st, (uint32_t)((q / S) & 1));

@@ -66,14 +66,11 @@ constexpr int kStages = BWM_STAGES;             // stage ring depth per warp (TM
 #define BWM_LAZY_CROSS 1   // LEAN: first-crossing search once per stage from the running max
 #endif
 constexpr bool kMirror = BWM_RING_MIRROR != 0;
-#ifndef BWM_PF_AHEAD
-#define BWM_PF_AHEAD 0     // CTA-wide L2 prefetch this many stages ahead of a warp's TMA issue (0: off;
-#endif                     // measured 2.2x SLOWER at C2 with 4 stages, every warp)
-#ifndef BWM_SYNC_EVERY
-#define BWM_SYNC_EVERY 0   // named CTA barrier every this many stages (power of 2; 0: free-running warps)
+#ifndef BWM_SHARED_BOX
+#define BWM_SHARED_BOX 0   // 1: one CTA-wide 256-px box per stage (1 KB rows), re-armed by the last warp to release it
 #endif
-#ifndef BWM_PF_ALL
-#define BWM_PF_ALL 1       // every warp prefetches (robust to warp drift); 0: warp 0 only
+#ifndef BWM_LAGT_WARPS
+#define BWM_LAGT_WARPS 4   // warps per CTA of the lagging-cursor kernel with smem tables (tables shared by all)
 #endif
 // the lagging-cursor mode moves two boxes per stage (dates t and t-h): 3 stages = 6 boxes
 // (kRingLag: tables in global memory, 3 stages, 3 CTAs/SM; kRingLagT: tables in smem, 2 stages,
@@ -135,7 +132,7 @@ __device__ __forceinline__ void tma_box_elect(uint32_t dst, const CUtensorMap* m
         : "memory");
 }
 __device__ __forceinline__ void tma_box2_elect(uint32_t dst, const CUtensorMap* map, int x, int y, int y2,
-                                               uint32_t bar, uint32_t bytes) {
+                                               uint32_t bar, uint32_t bytes, uint32_t box_bytes = kBoxBytes) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "elect.sync _|p, 0xffffffff;\n\t"
@@ -152,21 +149,8 @@ __device__ __forceinline__ void tma_box2_elect(uint32_t dst, const CUtensorMap* 
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%1], [%2, {%3, %7}], [%5];\n\t"
 #endif
         "}" ::"r"(dst),
-        "r"(dst + (uint32_t)(kStageRows * kWarpPx * 4)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
+        "r"(dst + box_bytes), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
         "r"(bar), "r"(bytes), "r"(y2)
-        : "memory");
-}
-
-// L2 prefetch of a (256 px, R dates) box of the CTA's tile: DRAM sees the tile's 1 KB row
-// segments together even when the four warps' own 64-px boxes are issued at different times
-// (free-running 64-px boxes stream at 3.6 TB/s, 256-px boxes at 7.2 TB/s:
-// profiles/probe/tma_probe_r01.txt); the per-warp TMA loads that follow hit L2.
-__device__ __forceinline__ void tma_prefetch_elect(const CUtensorMap* map, int x, int y) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "elect.sync _|p, 0xffffffff;\n\t"
-        "@p cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n\t"
-        "}" ::"l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y)
         : "memory");
 }
 
@@ -216,23 +200,39 @@ __device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
                  : "memory");
 }
 
-// Shared-memory footprint per warp stage (host mirror in bwm_capi.cu).
-__host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
-    return (int64_t)kBoxBytes * (mode == kRingLag || mode == kRingLagT ? 2 : 1);
-}
-
 #ifndef BWM_TMA_MINB
 #define BWM_TMA_MINB 4
 #endif
 #ifndef BWM_TMA_MINB_BIG
 #define BWM_TMA_MINB_BIG 3
 #endif
+// Warps per CTA: 4, or BWM_LAGT_WARPS for the lagging cursor with staged tables (C4: the 64 KB
+// Z^T table is shared by more warps, so more warps fit per SM); the tile is 64 px per warp.
+__host__ __device__ constexpr int tma_warps(int mode) { return mode == kRingLagT ? BWM_LAGT_WARPS : kWarps; }
+__host__ __device__ constexpr int tma_threads(int mode) { return 32 * tma_warps(mode); }
+__host__ __device__ constexpr int tma_tile(int mode) { return kWarpPx * tma_warps(mode); }
+__host__ __device__ constexpr int tma_minb(int np, int mode) {
+    return mode == kRingLagT ? (BWM_LAGT_WARPS > 4 ? 1 : 2) : np <= 10 ? BWM_TMA_MINB : BWM_TMA_MINB_BIG;
+}
+
+// Shared-memory footprint per warp stage (host mirror in bwm_capi.cu); with BWM_SHARED_BOX the
+// stages are CTA-wide (tma_stage_slots warps' worth each, one slot set per CTA).
+__host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
+    return (int64_t)kBoxBytes * (mode == kRingLag || mode == kRingLagT ? 2 : 1);
+}
+__host__ __device__ constexpr int64_t tma_stage_region(int mode, int stages) {
+    return (int64_t)tma_warps(mode) * stages * tma_stage_bytes(mode);   // same bytes either way
+}
+__host__ __device__ constexpr int tma_barriers(int mode, int stages) {
+    return BWM_SHARED_BOX ? stages : tma_warps(mode) * stages;
+}
+
 // LEAN: no MOSUM matrix / MOSUM mean outputs and a constant boundary over the monitoring
 // period (b_j = lambda for every j: log_plus((n+1+j)/n) = 1 while (n+1+j)/n <= e, which holds
 // for all BASELINE geometries, N/n = 2) — the per-date boundary product, mean accumulation
 // and output branch drop out of the MOSUM loop.  Results are bit-identical to !LEAN.
 template <int NP, int MODE, bool LEAN>
-__global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE == 3 /* kRingLagT */ ? 2 : BWM_TMA_MINB_BIG)
+__global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     monitor_kernel_tma(const __grid_constant__ KParams prm) {
     static_assert(MODE == kRingTmem || MODE == kRingLag || MODE == kRingLagT, "TMA kernel: TMEM ring or lagging cursor");
     constexpr bool kLag = MODE == kRingLag || MODE == kRingLagT;
@@ -240,27 +240,32 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
     constexpr int R = kStageRows;
     constexpr int S = stages_for(MODE);
     constexpr int64_t SB = tma_stage_bytes(MODE);
-    constexpr int ROWF2 = kWarpPx / 2;           // float2 per staged row of a warp slice
+    constexpr int NW = tma_warps(MODE), NT = tma_threads(MODE), TILE = tma_tile(MODE);
+    constexpr bool SHB = BWM_SHARED_BOX != 0;
+    constexpr int ROWF2 = (SHB ? TILE : kWarpPx) / 2;    // float2 per staged row
+    constexpr int64_t SBX = SHB ? SB * NW : SB;          // bytes of one stage slot
+    static_assert(MODE != kRingTmem || NW == 4, "TMEM ring: one TMEM lane quarter per warp");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
     const int NA = (N + 3) & ~3;
-    unsigned char* s_stage = smem_raw;                                   // [kWarps][S][SB]
+    unsigned char* s_stage = smem_raw;                                   // [NW][S][SB]
     // [N][SP] Z^T: fitted-value rows; for t < n they are the rows of Q (host: bwm_plan_create),
     // so pass 1 reads its basis from the same table (full stages only touch rows < n)
     // kRingLag (large h, C4): the tables stay in global memory and are read through L1 (uniform
     // addresses, broadcast) so that two CTAs fit per SM next to the double-box stage rings.
     constexpr bool kTblSmem = MODE != kRingLag;
-    float* s_tbl = reinterpret_cast<float*>(smem_raw + kWarps * S * SB);
+    float* s_tbl = reinterpret_cast<float*>(smem_raw + tma_stage_region(MODE, S));
     const float* s_xt = kTblSmem ? s_tbl : prm.xt;
     const float* s_mt = s_xt;
     float* s_bd = s_tbl + (kTblSmem ? N * SP : 0);                       // [NA] bound by row t (t >= n)
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);           // [kWarps][S]
-    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + kWarps * S);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);           // [NW][S] (SHB: [S])
+    uint32_t* s_tick = reinterpret_cast<uint32_t*>(s_bar + tma_barriers(MODE, S));   // SHB: [S] release tickets
+    uint32_t* s_tmem = s_tick + (SHB ? S : 0);
     int* s_rows = reinterpret_cast<int*>(s_tmem + 4);                   // [tile_stages] stage -> first date
 
     if (kTblSmem)
-        for (int i = threadIdx.x; i < N * SP; i += kTmaThreads) s_tbl[i] = prm.xt[i];
-    for (int i = threadIdx.x; i < N - n; i += kTmaThreads) s_bd[n + i] = prm.bound[i];
+        for (int i = threadIdx.x; i < N * SP; i += NT) s_tbl[i] = prm.xt[i];
+    for (int i = threadIdx.x; i < N - n; i += NT) s_bd[n + i] = prm.bound[i];
     {
         // the per-tile stage schedule (identical for every tile): pass 1 [0, n), pass 2 [w0, n)
         // (lagging-cursor mode only), pass 3 [8 floor(n/8), N), R dates per stage
@@ -268,11 +273,13 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         const int a = (n + kStageRows - 1) / kStageRows;
         const int b = a + (MODE == kRingTmem ? 0 : (n - w0_ + kStageRows - 1) / kStageRows);
         const int c = b + (N - t3_ + kStageRows - 1) / kStageRows;
-        for (int i = threadIdx.x; i < c; i += kTmaThreads)
+        for (int i = threadIdx.x; i < c; i += NT)
             s_rows[i] = i < a ? i * kStageRows : i < b ? w0_ + (i - a) * kStageRows : t3_ + (i - b) * kStageRows;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kWarps * S; ++s) mbar_init(s_bar + s, 1);
+        for (int s = 0; s < tma_barriers(MODE, S); ++s) mbar_init(s_bar + s, 1);
+        if (SHB)
+            for (int s = 0; s < S; ++s) s_tick[s] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (MODE == kRingTmem && threadIdx.x < 32) tmem_alloc(s_tmem, (uint32_t)prm.tmem_cols);
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
     __syncthreads();
     if (MODE == kRingTmem) tmem_fence_after();
 
-    const int64_t n_tiles = prm.n_pixels / kTile;      // host guarantees whole tiles
+    const int64_t n_tiles = prm.n_pixels / TILE;       // host guarantees whole tiles
     const int64_t ld = prm.ld_y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wstart = n - h + 1;                      // first row of MOSUM window 0 (mosum.py:59)
@@ -288,8 +295,8 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
     const int t3 = (n / R) * R;                        // first row of the (aligned) monitoring stream
     const int tid = threadIdx.x;
     const int wu = __shfl_sync(0xffffffffu, warp, 0);              // warp index, known warp-uniform
-    unsigned char* my_stage = s_stage + wu * S * SB;
-    uint64_t* full = s_bar + wu * S;
+    unsigned char* my_stage = SHB ? s_stage : s_stage + wu * S * SB;
+    uint64_t* full = SHB ? s_bar : s_bar + wu * S;
     const uint32_t stage_u32 = smem_u32(my_stage), bar_u32 = smem_u32(full);
 
     // ---- this warp's TMA issue cursor, kStages ahead of consumption ----------------------
@@ -304,44 +311,26 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
     // (tile, stage); the first date of a stage comes from the schedule table.
     int64_t itile = blockIdx.x;
     int istage = 0;
-    int xw = (int)(itile * kTile) + wu * kWarpPx;           // x of the cursor's tile slice
-    // L2 prefetch cursor: BWM_PF_AHEAD stages ahead of the issue cursor
-    constexpr int PF = BWM_PF_AHEAD;
-    const bool pf_warp = PF > 0 && (BWM_PF_ALL || wu == 0);
-    int64_t ptile = blockIdx.x;
-    int pstage = 0;
-    auto prefetch_next = [&]() {
-        if (ptile < n_tiles) {
-            const int r0 = s_rows[pstage];
-            tma_prefetch_elect(&prm.tmap_pf, (int)(ptile * kTile), r0);
-            if (kLag && pstage >= st1 + st2 && r0 >= h) tma_prefetch_elect(&prm.tmap_pf, (int)(ptile * kTile), r0 - h);
-        }
-        if (++pstage == tile_stages) {
-            pstage = 0;
-            ptile += gridDim.x;
-        }
-    };
-    auto issue_into = [&](int slot) {
-        if (pf_warp) prefetch_next();
+    int xw = (int)(itile * TILE) + (SHB ? 0 : wu * kWarpPx);   // x of the cursor's tile (slice)
+    constexpr uint32_t kBox = (uint32_t)(SHB ? kBoxBytes * NW : kBoxBytes);
+    auto issue_into = [&](int slot, bool really = true) {
         if (itile >= n_tiles) return;
-        const int r0 = s_rows[istage];
-        const uint32_t dst = stage_u32 + (uint32_t)(slot * SB), bar = bar_u32 + (uint32_t)(slot * 8);
-        if (kLag && istage >= st1 + st2)
-            tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBoxBytes);   // + dates t-h (<0: zero fill)
-        else
-            tma_box_elect(dst, &prm.tmap, xw, r0, bar, kBoxBytes);
+        if (really) {
+            const int r0 = s_rows[istage];
+            const uint32_t dst = stage_u32 + (uint32_t)(slot * SBX), bar = bar_u32 + (uint32_t)(slot * 8);
+            if (kLag && istage >= st1 + st2)
+                tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBox, kBox);   // + dates t-h (<0: zero fill)
+            else
+                tma_box_elect(dst, &prm.tmap, xw, r0, bar, kBox);
+        }
         if (++istage == tile_stages) {
             istage = 0;
             itile += gridDim.x;
-            xw += (int)gridDim.x * kTile;
+            xw += (int)gridDim.x * TILE;
         }
     };
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap)) : "memory");
-    if (pf_warp) {
-        if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap_pf)) : "memory");
-        for (int s = 0; s < PF; ++s) prefetch_next();       // then one per issue, PF stages ahead
-    }
-    for (int s = 0; s < S; ++s) issue_into(s);
+    for (int s = 0; s < S; ++s) issue_into(s, !SHB || wu == 0);
 
     const int L = prm.ring_rows;
     const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(wu * 32) << 16) : 0u;
@@ -399,19 +388,24 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         if (!next_ready) mbar_wait(full + cur, ph);
         const int nc = cur + 1 == S ? 0 : cur + 1;
         next_ready = mbar_test(full + nc, nc == 0 ? ph ^ 1 : ph);
-        return reinterpret_cast<const float2*>(my_stage + cur * SB) + lane;
+        return reinterpret_cast<const float2*>(my_stage + cur * SBX) + (SHB ? wu * (kWarpPx / 2) : 0) + lane;
     };
-    uint32_t n_rel = 0;
     auto release = [&]() {
-        if (BWM_SYNC_EVERY > 0 && ((++n_rel) & (BWM_SYNC_EVERY - 1)) == 0)
-            asm volatile("bar.sync 1, %0;" ::"n"(kTmaThreads) : "memory");   // keep the 4 warps' boxes coherent
         __syncwarp();
-        issue_into(cur);                             // re-arm this slot kStages ahead
+        bool mine = true;
+        if (SHB) {                                   // the last warp to release the slot re-arms it
+            uint32_t t = 0;
+            if (lane == 0) {
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(t) : "r"(smem_u32(s_tick + cur)) : "memory");
+            }
+            mine = (__shfl_sync(0xffffffffu, t, 0) % (uint32_t)NW) == (uint32_t)(NW - 1);
+        }
+        issue_into(cur, mine);                       // re-arm this slot kStages ahead
         if (++cur == S) { cur = 0; ph ^= 1; }
     };
 
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int64_t px0 = tile * kTile + 2 * tid;
+        const int64_t px0 = tile * TILE + 2 * tid;
         const float* yp = prm.y + px0;
 
         // ---- pass 1: beta_Q and ||y - c||^2 (+ pass 0 on the first stage) ---------------
@@ -583,7 +577,7 @@ __global__ void __launch_bounds__(kTmaThreads, NP <= 10 ? BWM_TMA_MINB : MODE ==
         int rb = q_t3h;                                  // ring row of t0 - h
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
-            const float2* lst = st + kBoxBytes / 8;      // lag dates (kRingLag): second box
+            const float2* lst = st + kBox / 8;           // lag dates (kRingLag): second box
             if (t0 >= n + (kLag ? 1 : 0) && t0 + R <= N) {
                 float2 oldv[R], newv[R];
                 if (MODE == kRingTmem) ring_load(rb, oldv);
