@@ -99,8 +99,8 @@ constexpr int kRingMaxH = 64;   // ring in smem up to h = 64 (64 KB); above: lag
 // shared memory of the LDG kernel: tables + MOSUM ring
 int64_t smem_bytes_for(int N, int n, int h, int p, bool ring) {
     const int sp = (p + 3) & ~3;
-    // ring variants stage the coefficient tables; lagging-cursor variants read them from L1
-    int64_t fl = (ring ? (int64_t)n * sp + (int64_t)N * sp : 0) + (((N - n) + 3) & ~3);
+    // ring variants stage the window-sum table; lagging-cursor variants read it from L1
+    int64_t fl = (ring ? (int64_t)N * sp : 0) + (((N - n) + 3) & ~3);   // window-sum table + bound
     int64_t bytes = fl * 4;
     if (ring) bytes += (int64_t)h * bwm::kThreads * 8;
     return bytes;
@@ -288,7 +288,10 @@ struct bwm_plan {
     bool force_ldg = false;            // BWM_KERNEL=ldg (A/B against the TMA kernel)
     bool const_bound = false;          // b_j == b_0 for every j (LEAN TMA variant applies)
     bool precise = false;              // long horizon: float64 fitted values, LDG kernels only
-    double* d_xtd = nullptr;           // [N][sp] Z^T in float64 (precise mode and the fixup)
+    double* d_xtd = nullptr;           // [N][sp] Z^T in float64 (the fixup)
+    float* d_wt = nullptr;             // [N][sp] window-sum table (rows < n: Q^T, rows >= n: S_t)
+    double* d_wtd = nullptr;           // the same in float64 (precise mode)
+    double s0 = 0.0;                   // h * z[0]: intercept part of every S_t
     // float64 fixup of ill-conditioned pixels (bwm_fixup.cu): device list + count, grown on use
     double lambda_d = 0.0;            // masked float64 kernel
     float fix_ratio = 300.f;     // ||y-c||^2 / RSS above which a pixel is recomputed in float64
@@ -345,6 +348,8 @@ static void plan_free_tables(bwm_plan* plan) {
     cudaFree(plan->d_bound);
     cudaFree(plan->d_rinv);
     cudaFree(plan->d_xtd);
+    cudaFree(plan->d_wt);
+    cudaFree(plan->d_wtd);
     cudaFree(plan->d_fix_list);
     cudaFree(plan->d_fix_count);
     cudaFree(plan->d_xx);
@@ -558,7 +563,8 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
             plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->tring.mode);
         }
         // lagging cursor: tables staged in smem when they fit (kRingLagT), else through L1
-        if (plan->tring.mode == (int)bwm::kRingLag &&
+        const char* l1_env = getenv("BWM_TMA_LAGL1");        // A/B: keep the L1-table variant
+        if (plan->tring.mode == (int)bwm::kRingLag && !(l1_env && std::strcmp(l1_env, "1") == 0) &&
             smem_bytes_tma(N, n, h, p, bwm::kRingLagT) <= std::min<int64_t>(optin, BWM_LAGT_WARPS > 4 ? optin : (110 << 10))) {
             plan->tring = {(int)bwm::kRingLagT, 0, 0};
             plan->smem_tma = smem_bytes_tma(N, n, h, p, plan->tring.mode);
@@ -656,6 +662,28 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
                 xtd[(size_t)t * sp + i] = t < n ? Q[(size_t)t * p + i] : z;
             }
     }
+    // Window-sum table (bwm_common.cuh, KParams::wt): rows t < n are q_t (pass 1), rows t >= n
+    // S_t = sum of z_s over the MOSUM window of date t, [t-h+1, t] (mosum.py:59), in float64.
+    // Design row 0 is the intercept (bwm_tables), so z_s[0] = 1/R00 for every s: S_t[0] is the
+    // constant s0 = h/R00, applied once to the initial window sum, and column 0 is stored as 0.
+    for (int t = 0; t < N; ++t)
+        if (tb->design[t] != 1.0) {
+            plan_free_tables(plan);
+            delete plan;
+            return set_err(BWM_E_DIMS, "design row 0 must be the intercept (1.0 at every date)");
+        }
+    std::vector<double> wtd((size_t)N * sp, 0.0);
+    for (int t = 0; t < n; ++t)
+        for (int i = 0; i < p; ++i) wtd[(size_t)t * sp + i] = Q[(size_t)t * p + i];
+    for (int t = n; t < N; ++t)
+        for (int i = 1; i < p; ++i) {
+            double s = 0.0;
+            for (int u = t - h + 1; u <= t; ++u) s += xtd[(size_t)u * sp + i];
+            wtd[(size_t)t * sp + i] = s;
+        }
+    plan->s0 = (double)h * Rinv[0];
+    std::vector<float> wt(wtd.size());
+    for (size_t i = 0; i < wt.size(); ++i) wt[i] = (float)wtd[i];
 
     auto fail = [&](cudaError_t e, const char* what) {
         plan_free_tables(plan);
@@ -679,6 +707,14 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     {
         if ((e = cudaMalloc(&plan->d_xtd, xtd.size() * 8)) != cudaSuccess) return fail(e, "cudaMalloc");
         if ((e = cudaMemcpy(plan->d_xtd, xtd.data(), xtd.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return fail(e, "cudaMemcpy");
+    }
+    if ((e = cudaMalloc(&plan->d_wt, wt.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMemcpy(plan->d_wt, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy");
+    if (plan->precise) {
+        if ((e = cudaMalloc(&plan->d_wtd, wtd.size() * 8)) != cudaSuccess) return fail(e, "cudaMalloc");
+        if ((e = cudaMemcpy(plan->d_wtd, wtd.data(), wtd.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess)
             return fail(e, "cudaMemcpy");
     }
 
@@ -852,6 +888,9 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     k.ld_out = out->ld_out;
     k.zero_sigma = reinterpret_cast<unsigned long long*>(out->zero_sigma_pixel);
     k.xtd = plan->precise ? plan->d_xtd : nullptr;
+    k.wt = plan->d_wt;
+    k.wtd = plan->precise ? plan->d_wtd : nullptr;
+    k.s0 = plan->s0;
     cudaStream_t st = (cudaStream_t)stream;
     int launched = 0;
     // float64 fixup list for ill-conditioned pixels (fill mode, float32 kernels)

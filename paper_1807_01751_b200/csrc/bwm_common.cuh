@@ -67,6 +67,17 @@ struct KParams {
     // tensor-core fitted values (bwm_kernel_mma.cuh): Z^T split into tf32 hi/lo B tables
     const float* zb_cur;        // current dates [w0, ...)
     const float* zb_lag;        // lag dates [t3 - h, ...)
+    // window-sum formulation (TMA and LDG kernels): the MOSUM window sum of residuals is
+    //   sum_{s in window(t)} r_s = sum_{s in window(t)} (y_s - c) - S_t^T beta_Q,
+    //   S_t = sum_{s in window(t)} z_s  (host, float64),
+    // linear in y, so the monitoring pass carries the window sum of the FILLED series and one
+    // dot with S_t per date, and neither the lagged date nor window 0 needs a fitted value.
+    // Design row 0 is the intercept, so z_t[0] = 1/R00 for every t and S_t[0] = s0 = h/R00:
+    // that part enters the initial window sum once, in float64 (it also centres the running
+    // sum on the history mean), and the per-date dot covers k >= 1.
+    const float* wt;            // [N][sp] rows t < n: q_t (Q^T); rows t >= n: S_t (column 0 = 0)
+    const double* wtd;          // the same table in float64 (precise mode), or nullptr
+    double s0;                  // h * z[0]
 };
 
 // append pixel `px` (launch-relative) to the fixup list when its history fit is ill-conditioned:
@@ -135,6 +146,29 @@ __device__ __forceinline__ float2 dot_row(float2 r, const float* __restrict__ xr
         if (4 * q + 3 < NP) r = fma2s(nb[4 * q + 3], x.w, r);
     }
     return r;
+}
+
+// Numerator of MO_t in the window-sum formulation: acc + sum_{k >= 1} nb_k * S_t[k]
+// (nb = -beta_Q; S_t[0] is folded into acc).  Same FFMA2 chain order as dot_row.
+template <int NP, int SP>
+__device__ __forceinline__ float2 wsum_row(float2 acc, const float* __restrict__ srow, const float2 (&nb)[NP]) {
+    const float4* s4 = reinterpret_cast<const float4*>(srow);
+#pragma unroll
+    for (int q = 0; q < SP / 4; ++q) {
+        const float4 s = s4[q];
+        if (q > 0 && 4 * q + 0 < NP) acc = fma2s(nb[4 * q + 0], s.x, acc);
+        if (4 * q + 1 < NP) acc = fma2s(nb[4 * q + 1], s.y, acc);
+        if (4 * q + 2 < NP) acc = fma2s(nb[4 * q + 2], s.z, acc);
+        if (4 * q + 3 < NP) acc = fma2s(nb[4 * q + 3], s.w, acc);
+    }
+    return acc;
+}
+
+// Initial window sum (window of date n minus its newest date: dates [n-h, n), h of them) minus
+// the intercept part s0 * beta_Q[0], in float64 — the ỹ sum w and beta_Q[0] = hi + lo are
+// large and nearly equal after a level shift, their difference is the residual window sum.
+__device__ __forceinline__ float2 wsum_init(double w0, double w1, float2 hi0, float2 lo0, double s0) {
+    return f2((float)(w0 - s0 * ((double)hi0.x + (double)lo0.x)), (float)(w1 - s0 * ((double)hi0.y + (double)lo0.y)));
 }
 
 // r = y_c - z^T beta_Q with z from the float64 table and beta_Q = hi + lo in float64 (precise mode)

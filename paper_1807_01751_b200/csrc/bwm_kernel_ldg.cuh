@@ -11,29 +11,29 @@
 //   ingest  _ingest_block  (305-319)            pass 0: first finite value c per pixel
 //                                               fill on the fly: NaN/Inf -> last finite value,
 //                                               leading gap -> c (exact float32 copies)
-//   model   M @ values[:n]  (339-349)           pass 1: beta' = M'(y - c), FFMA2, blocks of
-//                                               16 dates 2Sum-compensated into (hi, lo)
-//   predictions / residuals (351-385)           pass 2: r_t = (y_t - c) - x'_t beta', sigma^2
-//   mosum  _kernels.mosum_block (21-34)         pass 3: window recurrence acc += r_new - r_old
+//   model   M @ values[:n]  (339-349)           pass 1: beta_Q = Q^T (y - c), FFMA2, 32-date
+//                                               blocks 2Sum-compensated into (hi, lo); the
+//                                               window sum of the filled dates [n-h, n)
+//   predictions / residuals (351-385)           sigma from RSS = ||y-c||^2 - ||beta_Q||^2;
+//                                               window-sum formulation (bwm_common.cuh): the
+//                                               fitted values enter only as S_t^T beta_Q
+//   mosum  _kernels.mosum_block (21-34)         pass 3: window recurrence acc += y~_new - y~_old
 //   breaks _kernels.detect_block (37-48)                 |MO| max, first strict crossing
 //
 // Memory: the stack is time-major (row t = every pixel at date t), so a warp reading one
 // date of its 64 pixels issues one coalesced 256-byte request (float2 per lane).  Rows are
-// streamed through a 16-deep per-thread register ring; refills run across pass
-// boundaries and into the next tile, so the load pipe never drains between passes.
-// Pass 2 re-reads the history rows pass 1 read moments earlier; they are L2-resident
-// (re-read footprint ~117 KB per resident CTA, ~70 MB chip-wide, L2 = 126 MB), so HBM
-// reads each element of y once.
-//
-// Numerics: see bwm_common.cuh.
+// streamed through a 16-deep per-thread register ring (slot t mod 16 holds row t), in ONE
+// sweep over the dates per tile; refills run across the pass boundary and into the next
+// tile's first rows, so the load pipe never drains.  Every operation matches the TMA kernel's
+// order, so both give bit-identical results (test_kernel_variants_bit_identical).
 #pragma once
 
 #include "bwm_common.cuh"
 
 namespace bwm {
 
-// RING = true : r_{t-h} comes from a per-thread smem ring of h residuals (h*1 KB per CTA).
-// RING = false: r_{t-h} is recomputed from y_{t-h} by a lagging cursor (an L2 hit: that row
+// RING = true : y~_{t-h} comes from a per-thread smem ring of h filled values (h*1 KB per CTA).
+// RING = false: y~_{t-h} is refilled from y_{t-h} by a lagging cursor (an L2 hit: that row
 //               was read h rows earlier) — used when the ring would not fit (large h, C4).
 template <int NP, bool SAFE, bool RING>
 __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams prm) {
@@ -41,20 +41,17 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
     constexpr int D = kDepth;
     extern __shared__ __align__(16) float smem[];
     const int N = prm.N, n = prm.n, h = prm.h;
-    // RING: the coefficient tables live in smem.  !RING (large h or long series): they stay
-    // in global memory, read through L1 (uniform addresses), so any N fits; only the
-    // boundary is staged.
+    // RING: the window-sum table (rows < n: Q^T, rows >= n: S_t) lives in smem.  !RING (large
+    // h or long series): it stays in global memory, read through L1 (uniform addresses), so
+    // any N fits; only the boundary is staged.
     float* s_tab = smem;
-    const float* s_mt = RING ? s_tab : prm.mt;                                 // [n][SP]
-    const float* s_xt = RING ? s_tab + n * SP : prm.xt;                        // [N][SP]
-    float* s_bd = s_tab + (RING ? (n + N) * SP : 0);                           // [N-n] (padded to 4)
+    const float* s_wt = RING ? s_tab : prm.wt;                                 // [N][SP]
+    float* s_bd = s_tab + (RING ? N * SP : 0);                                 // [N-n] (padded to 4)
     float2* s_ring = reinterpret_cast<float2*>(s_bd + ((N - n + 3) & ~3));   // [h][kThreads]
 
     // --- constant tables -> smem (once per persistent CTA) -------------------------
-    if (RING) {
-        for (int i = threadIdx.x; i < n * SP; i += kThreads) s_tab[i] = prm.mt[i];
-        for (int i = threadIdx.x; i < N * SP; i += kThreads) s_tab[n * SP + i] = prm.xt[i];
-    }
+    if (RING)
+        for (int i = threadIdx.x; i < N * SP; i += kThreads) s_tab[i] = prm.wt[i];
     for (int i = threadIdx.x; i < N - n; i += kThreads) s_bd[i] = prm.bound[i];
     __syncthreads();
 
@@ -63,7 +60,8 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
     const int64_t n_tiles = (prm.n_pixels + kTile - 1) / kTile;
     const int64_t ld = prm.ld_y;
     const int64_t hld = (int64_t)h * ld;
-    const int wstart = n - h + 1;             // first row of MOSUM window 0 (mosum.py:59)
+    const int wst = n - h;                    // first date of the initial window [n-h, n)
+    const double* const wtd = prm.wtd;        // precise mode: float64 table (long horizons)
 
     int64_t tile = blockIdx.x;
     if (tile >= n_tiles) return;
@@ -71,10 +69,13 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
     int npx = SAFE ? (int)max((int64_t)0, min((int64_t)2, prm.n_pixels - px0)) : 2;
     const float* yp = prm.y + px0;
 
-    float2 buf[D];
+    float2 buf[D];                            // slot t mod D: row t
+    float2 lbuf[RING ? 1 : D];                // !RING, slot t mod D: row t - h (t >= n)
 #pragma unroll
-    for (int k = 0; k < D; ++k)
-        if (k < n) buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);
+    for (int k = 0; k < D; ++k) {
+        if (k < N) buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);
+        if (!RING && k >= n && k < N) lbuf[RING ? 0 : k] = ldp<SAFE>(yp + (int64_t)(k - h) * ld, npx);
+    }
 
     for (;;) {
         const int64_t next_tile = tile + gridDim.x;
@@ -82,6 +83,21 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         const int64_t npx0 = has_next ? next_tile * kTile + 2 * tid : px0;
         const int nnpx = SAFE ? (has_next ? (int)max((int64_t)0, min((int64_t)2, prm.n_pixels - npx0)) : 0) : 2;
         const float* ynp = prm.y + npx0;
+
+        // Consume row t (slot k = t mod D): refill the slot with row t + D of this tile, or,
+        // past the last row, with row k of the next tile; the lag slot likewise with row
+        // t + D - h (monitoring rows only).  pf points at row t + D.
+        const float* pf = yp + (int64_t)D * ld;
+        auto refill = [&](const int k, const int t) {
+            if (t + D < N) {
+                buf[k] = ldp<SAFE>(pf, npx);
+                if (!RING && t + D >= n) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
+            } else if (has_next && k < N) {
+                buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);
+                if (!RING && k >= n) lbuf[RING ? 0 : k] = ldp<SAFE>(ynp + (int64_t)(k - h) * ld, nnpx);
+            }
+            pf += ld;
+        };
 
         // ---- pass 0: first finite value per pixel (warp-cooperative early exit) -----
         float2 c = f2(0.f, 0.f);
@@ -103,47 +119,56 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         const bool valid1 = (npx >= 2) && f1;
         const float2 negc = f2(-c.x, -c.y);
 
-        // ---- pass 1: beta' = M' (y - c), 2Sum-compensated 16-date blocks ------------
+        // ---- pass 1: beta_Q, ||y - c||^2, the initial window sum -----------------------
         float2 hi[NP], lo[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) { hi[i] = f2(0.f, 0.f); lo[i] = f2(0.f, 0.f); }
-        double q0 = 0.0, q1 = 0.0;           // ||y - c||^2 (16-date float32 partials, float64 sum)
-        float2 last = f2(0.f, 0.f);
-        const float* pf = yp + (int64_t)D * ld;   // refill target of the row being consumed
-        float2 part[NP], qpart = f2(0.f, 0.f);
+        double q0 = 0.0, q1 = 0.0;           // ||y - c||^2 (32-date float32 partials, float64 sum)
+        double wd0 = 0.0, wd1 = 0.0;         // window sum of [n-h, n), same blocks
+        float2 last = f2(0.f, 0.f), lag_last = f2(0.f, 0.f);
+        float2 part[NP], qpart = f2(0.f, 0.f), wpart = f2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < NP; ++i) part[i] = f2(0.f, 0.f);
+        int slot = RING ? wst % h : 0;       // RING: ring slot of date t is t mod h
         // precise mode (long horizons): beta_Q and ||y - c||^2 also accumulated in float64 — the
-        // float32 block partials' rounding, multiplied by a far-extrapolated z_t, is what limits
-        // the fitted value there
-        const double* const xtd = prm.xtd;
+        // float32 block partials' rounding, multiplied by a far-extrapolated S_t, is what limits
+        // the MOSUM there
         double pd0[NP], pd1[NP], qd0 = 0.0, qd1 = 0.0;
 #pragma unroll
         for (int i = 0; i < NP; ++i) pd0[i] = pd1[i] = 0.0;
-        auto acc_f64 = [&](float2 vc, int t) {
-            if (!xtd) return;
-            const double a = (double)vc.x, b = (double)vc.y;
-            const double* z = xtd + (int64_t)t * SP;
-#pragma unroll
-            for (int i = 0; i < NP; ++i) {
-                const double zz = __ldg(z + i);
-                pd0[i] = fma(a, zz, pd0[i]);
-                pd1[i] = fma(b, zz, pd1[i]);
+        auto hist_row = [&](const float2 v, const int t) {
+            const float2 vc = fill(v, negc, last);
+            axpy_row<NP, SP>(part, vc, s_wt + t * SP);
+            qpart = fma2(vc, vc, qpart);
+            if (t >= wst) {
+                wpart = add2(wpart, vc);
+                if (RING) {
+                    ring[slot * kThreads] = vc;
+                    slot = (slot + 1 == h) ? 0 : slot + 1;
+                }
             }
-            qd0 = fma(a, a, qd0);
-            qd1 = fma(b, b, qd1);
+            if (!RING && t == wst - 1) lag_last = vc;
+            if (wtd) {
+                const double a = (double)vc.x, b = (double)vc.y;
+                const double* z = wtd + (int64_t)t * SP;
+#pragma unroll
+                for (int i = 0; i < NP; ++i) {
+                    const double zz = __ldg(z + i);
+                    pd0[i] = fma(a, zz, pd0[i]);
+                    pd1[i] = fma(b, zz, pd1[i]);
+                }
+                qd0 = fma(a, a, qd0);
+                qd1 = fma(b, b, qd1);
+            }
         };
         for (int t0 = 0; t0 < n; t0 += D) {
-            if (t0 + 2 * D <= n) {
+            if (t0 + 2 * D <= n) {            // every refill row is a history row: no lag loads
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
                     const float2 v = buf[k];
                     buf[k] = ldp<SAFE>(pf, npx);
                     pf += ld;
-                    const float2 vc = fill(v, negc, last);
-                    axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
-                    qpart = fma2(vc, vc, qpart);
-                    acc_f64(vc, t0 + k);
+                    hist_row(v, t0 + k);
                 }
             } else {
 #pragma unroll
@@ -151,15 +176,8 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                     const int t = t0 + k;
                     if (t < n) {
                         const float2 v = buf[k];
-                        if (t + D < n) buf[k] = ldp<SAFE>(pf, npx);        // next pass-1 row
-                        else if (k < N) buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);  // pass-2 row k
-                        pf += ld;
-                        const float2 vc = fill(v, negc, last);
-                        axpy_row<NP, SP>(part, vc, s_mt + t * SP);
-                        qpart = fma2(vc, vc, qpart);
-                        acc_f64(vc, t);
-                    } else if (k < N) {
-                        buf[k] = ldp<SAFE>(yp + (int64_t)k * ld, npx);      // free slot: pass-2 row k
+                        refill(k, t);
+                        hist_row(v, t);
                     }
                 }
             }
@@ -168,78 +186,47 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                 for (int i = 0; i < NP; ++i) { two_sum(hi[i], lo[i], part[i]); part[i] = f2(0.f, 0.f); }
                 q0 += (double)qpart.x;
                 q1 += (double)qpart.y;
-                qpart = f2(0.f, 0.f);
+                wd0 += (double)wpart.x;
+                wd1 += (double)wpart.y;
+                qpart = wpart = f2(0.f, 0.f);
             }
         }
         float2 bq[NP], nb[NP];    // beta_Q and -beta_Q
-        double bd0[NP], bd1[NP];  // precise mode: beta_Q in float64
         double sd0 = 0.0, sd1 = 0.0;
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             bq[i] = add2(hi[i], lo[i]);
             nb[i] = f2(-bq[i].x, -bq[i].y);
-            bd0[i] = pd0[i];
-            bd1[i] = pd1[i];
             sd0 = fma(pd0[i], pd0[i], sd0);
             sd1 = fma(pd1[i], pd1[i], sd1);
         }
-        // residual of date t (float32 fitted value, or float64 for long horizons: uniform branch)
-        auto resid = [&](float2 vc, int t) -> float2 {
-            if (xtd) return resid_f64<NP, SP>(vc, xtd + (int64_t)t * SP, bd0, bd1);
-            return dot_row<NP, SP>(vc, s_xt + t * SP, nb);
-        };
-        const float2 ss = xtd ? f2((float)fmax(qd0 - sd0, 0.0), (float)fmax(qd1 - sd1, 0.0))
+        const float2 ss = wtd ? f2((float)fmax(qd0 - sd0, 0.0), (float)fmax(qd1 - sd1, 0.0))
                               : rss_onepass<NP>(q0, q1, bq);
-        if (!xtd) {
+        if (!wtd) {
             fix_flag(prm, valid0, q0, ss.x, px0);
             fix_flag(prm, valid1, q1, ss.y, px0 + 1);
         }
-
-        // ---- pass 2: fill state through the history; residuals of window 0 --------------
-        float2 acc = f2(0.f, 0.f);
-        last = f2(0.f, 0.f);
-        float2 lag_last = f2(0.f, 0.f);          // !RING: fill state of the lagging cursor
-        float2 lbuf[RING ? 1 : D];               // !RING: prefetched rows t+D-h
-        int slot = wstart % h;                   // ring slot of row t is t mod h
-        pf = yp + (int64_t)D * ld;
-        for (int t0 = 0; t0 < n; t0 += D) {
-            if (t0 + D < wstart && t0 + 2 * D <= N) {
+        // initial window sum minus the intercept part of S^T beta_Q (float64)
+        float2 acc = wtd ? f2((float)(wd0 - prm.s0 * pd0[0]), (float)(wd1 - prm.s0 * pd1[0]))
+                         : wsum_init(wd0, wd1, hi[0], lo[0], prm.s0);
+        // MOSUM numerator of date t: acc - S_t^T beta_Q (float64 for long horizons: uniform branch)
+        auto numer = [&](const float2 a, const int t) -> float2 {
+            if (wtd) {
+                const double* s = wtd + (int64_t)t * SP;
+                double r0 = (double)a.x, r1 = (double)a.y;
 #pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const float2 v = buf[k];
-                    buf[k] = ldp<SAFE>(pf, npx);
-                    pf += ld;
-                    fill(v, negc, last);        // rows before window 0: fill state only
+                for (int i = 1; i < NP; ++i) {
+                    const double z = __ldg(s + i);
+                    r0 = fma(-z, pd0[i], r0);
+                    r1 = fma(-z, pd1[i], r1);
                 }
-            } else {
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const int t = t0 + k;
-                    if (t < n) {
-                        const float2 v = buf[k];
-                        if (t + D < N) buf[k] = ldp<SAFE>(pf, npx);
-                        else if (has_next && k < n) buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);
-                        if (!RING && t + D > n && t + D < N) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
-                        pf += ld;
-                        const float2 vc = fill(v, negc, last);
-                        if (t >= wstart) {
-                            const float2 r = resid(vc, t);
-                            acc = add2(acc, r);
-                            if (RING) {
-                                ring[slot * kThreads] = r;
-                                slot = (slot + 1 == h) ? 0 : slot + 1;
-                            }
-                        }
-                        if (!RING && t == wstart - 1) lag_last = last;
-                    }
-                }
+                return f2((float)r0, (float)r1);
             }
-        }
-        // slot == n mod h now: the slot of r_{n-h}, which window 0 does not contain
-        if (RING) ring[slot * kThreads] = f2(0.f, 0.f);
+            return wsum_row<NP, SP>(a, s_wt + t * SP, nb);
+        };
 
         // sigma and the zero-sigma contract: see bwm_kernel_tma.cuh (identical arithmetic)
-        const bool z0 = zero_history(valid0, xtd ? qd0 : q0, c.x), z1 = zero_history(valid1, xtd ? qd1 : q1, c.y);
+        const bool z0 = zero_history(valid0, wtd ? qd0 : q0, c.x), z1 = zero_history(valid1, wtd ? qd1 : q1, c.y);
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
         const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);
         const float2 inv = inv_scale(sc);
@@ -249,49 +236,51 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
         int first0 = 0x7fffffff, first1 = 0x7fffffff;
         float* const mo_out = prm.mosum;
         const bool want_sup = prm.sup != nullptr;
-        // one monitoring row; fast: no bounds checks, refill is the same pass's row t+D
+        // one monitoring row; fast: no bounds checks, refill is the same tile's row t+D
         auto mon_row = [&](const int k, const int t, const bool fast) {
             const float2 v = buf[k];
-            if (fast || t + D < N) buf[k] = ldp<SAFE>(pf, npx);
-            else if (has_next && k < n) buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);
-            float2 old = f2(0.f, 0.f);
-            const float2 r = resid(fill(v, negc, last), t);
+            float2 lv = f2(0.f, 0.f);
+            if (!RING) lv = lbuf[RING ? 0 : k];
+            if (fast) {
+                buf[k] = ldp<SAFE>(pf, npx);
+                if (!RING) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
+                pf += ld;
+            } else {
+                refill(k, t);
+            }
+            const float2 r = fill(v, negc, last);
+            float2 old;
             if (RING) {
                 old = ring[slot * kThreads];
                 ring[slot * kThreads] = r;
                 slot = (slot + 1 == h) ? 0 : slot + 1;
             } else {
-                if (fast || t > n) {     // r_{t-h}; at t == n, r_{n-h} is outside window 0
-                    const float2 lv = (fast || t >= D) ? lbuf[RING ? 0 : k]
-                                                       : ldp<SAFE>(pf - (int64_t)D * ld - hld, npx);
-                    old = resid(fill(lv, negc, lag_last), t - h);
-                }
-                if (fast || t + D < N) lbuf[RING ? 0 : k] = ldp<SAFE>(pf - hld, npx);
+                old = fill(lv, negc, lag_last);
             }
-            pf += ld;
             acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
+            const float2 num = numer(acc, t);
             const int j = t - n;
             const float bj = s_bd[j];
             const float2 bs = mul2(sc, f2(bj, bj));    // boundary in the unscaled frame
-            const float a0 = fabsf(acc.x), a1 = fabsf(acc.y);
+            const float a0 = fabsf(num.x), a1 = fabsf(num.y);
             mx.x = fmaxf(mx.x, a0);
             mx.y = fmaxf(mx.y, a1);
             if (a0 > bs.x) first0 = min(first0, j + 1);  // strict crossing (_kernels.py:47)
             if (a1 > bs.y) first1 = min(first1, j + 1);
-            if (want_sup) {                              // max_j |acc_j| / b_j (unscaled)
+            if (want_sup) {                              // max_j |num_j| / b_j (unscaled)
                 sr.x = fmaxf(sr.x, __fdividef(a0, bj));
                 sr.y = fmaxf(sr.y, __fdividef(a1, bj));
             }
-            msum = add2(msum, acc);
+            msum = add2(msum, num);
             if (mo_out) {
-                const float2 mo = mul2(acc, inv);
+                const float2 mo = mul2(num, inv);
                 float* o = mo_out + (int64_t)j * prm.ld_out + px0;
                 if (npx >= 1) o[0] = mo.x;
                 if (npx >= 2) o[1] = mo.y;
             }
         };
         for (int t0 = (n / D) * D; t0 < N; t0 += D) {
-            if (t0 > n && t0 + 2 * D <= N) {
+            if (t0 >= n && t0 + 2 * D <= N) {
 #pragma unroll
                 for (int k = 0; k < D; ++k) mon_row(k, t0 + k, true);
             } else {
@@ -299,8 +288,6 @@ __global__ void __launch_bounds__(kThreads, 2) monitor_kernel_ldg(const KParams 
                 for (int k = 0; k < D; ++k) {
                     const int t = t0 + k;
                     if (t >= n && t < N) mon_row(k, t, false);
-                    else if (t >= N && has_next && k < n)
-                        buf[k] = ldp<SAFE>(ynp + (int64_t)k * ld, nnpx);   // free slot: next tile
                 }
             }
         }

@@ -108,7 +108,7 @@ template <int NP, bool LEAN>
 __global__ void __launch_bounds__(kMmaThreads, 1) monitor_kernel_mma(const __grid_constant__ KParams prm) {
     constexpr int SP = Coefs<NP>::SP;
     constexpr int R = kStageRows;
-    static_assert(R == 8, "MMA kernel: 8-date stages (two per 16-date chunk)");
+    static_assert(R == 8 || NP < 0, "MMA kernel: 8-date stages (two per 16-date chunk)");
     constexpr int S = kMmaS;
     constexpr int64_t SB = kMmaStageBytes;
     constexpr int KS = mma_ks(NP), AC = mma_a_cols(NP), NB = kMmaNB;

@@ -13,25 +13,28 @@
 //   pass 1 : rows [0, n)             beta_Q = Q^T (y - c) and ||y - c||^2 in ONE sweep
 //                                    (pass 0 scans the first stage for c); sigma follows from
 //                                    RSS = ||y-c||^2 - ||beta_Q||^2 (orthonormal basis Q).
-//                                    TMEM mode also parks the filled dates [w0, n) in the ring;
-//                                    once beta is known they become the window-0 residuals
-//                                    in place (no re-read), w0 = 8*floor((n-h+1)/8)
-//   pass 2 : rows [w0, n)            LAG mode only: the window-0 rows again (L2 hits)
+//                                    Also the window sum of the filled dates [n-h, n) and (TMEM
+//                                    mode) those dates parked in the ring.
 //   pass 3 : rows [8*floor(n/8), N)  MOSUM recurrence + detect (stages 8-date aligned);
-//            LAG mode: each stage also carries dates t-h (second box; t-h < 0 is OOB zero fill)
+//            LAG mode: each stage also carries dates t-h (second box)
+// Window-sum formulation (bwm_common.cuh, KParams::wt): the recurrence runs on the FILLED
+// series, acc += y~_t - y~_{t-h} (_kernels.py:33 order), and the MOSUM numerator of date t is
+// acc - S_t^T beta_Q, S_t the window sum of the fitted-value rows (host table).  So the
+// history is read once (no window-0 re-read or conversion), and the lagged date needs no
+// fitted value — at C4 (h = 250, p = 14) that halves the FMA work of the monitoring period.
 // Measured (profiles/probe): SM-side ingest, DRAM or L2, saturates near 7 TB/s, so re-reading
 // the whole history (342 rows/tile) cost ~1 ms at C2; the TMEM-mode stream is 232 rows/tile.
 //
-// MOSUM residual ring (r_{t-h} for the add-one/drop-one recurrence, _kernels.py:31-34):
+// MOSUM ring (y~_{t-h} for the add-one/drop-one recurrence, _kernels.py:31-34):
 //   MODE kRingTmem : in Tensor Memory.  Each thread owns its TMEM lane; ring row q of the
 //                    pixel pair occupies columns 2q, 2q+1; L = ring rows (multiple of the
 //                    stage height R, >= h), plus R MIRROR rows L..L+R-1 that duplicate rows
 //                    0..R-1 (every write of a row < R also writes row q + L), so the R lagged
 //                    rows of a stage are always one contiguous run: R/8 tcgen05.st.x16 and R/8
 //                    tcgen05.ld.x16 per stage, no wrap path.  2(L+R) columns: 128 at h <= 56.
-//   MODE kRingLag  : no ring; r_{t-h} recomputed from the staged date t-h (large h); tables
-//                    read through L1 (any series length).  kRingLagT: the same with the tables
-//                    staged in shared memory (when they fit).
+//   MODE kRingLag  : no ring; y~_{t-h} refilled from the staged date t-h (large h) by a
+//                    lagging fill cursor; tables read through L1 (any series length).
+//                    kRingLagT: the same with the tables staged in shared memory (when they fit).
 //   (h < R, where an R-row batch would read rows it has not written yet, runs the LDG kernel.)
 //
 // The monitoring pass runs in the UNSCALED frame: acc = sum of window residuals, crossing
@@ -75,8 +78,11 @@ constexpr bool kMirror = BWM_RING_MIRROR != 0;
 // the lagging-cursor mode moves two boxes per stage (dates t and t-h): 3 stages = 6 boxes
 // (kRingLag: tables in global memory, 3 stages, 3 CTAs/SM; kRingLagT: tables in smem, 2 stages,
 //  2 CTAs/SM — measured 8.85 vs 8.11 ms at C4, so kRingLagT whenever its tables fit)
+#ifndef BWM_STAGES_LAGT
+#define BWM_STAGES_LAGT 2
+#endif
 __host__ __device__ constexpr int stages_for(int mode) {
-    return mode == 2 /* kRingLag */ ? BWM_STAGES_LAG : mode == 3 /* kRingLagT */ ? 2 : kStages;
+    return mode == 2 /* kRingLag */ ? BWM_STAGES_LAG : mode == 3 /* kRingLagT */ ? BWM_STAGES_LAGT : kStages;
 }
 static_assert(kStageRows == 8 || kStageRows == 16, "stage height: 8 or 16 dates (compensation blocks are 16)");
 constexpr int kWarpPx = 64;                     // pixels per warp slice (32 lanes x 2)
@@ -129,6 +135,22 @@ __device__ __forceinline__ void tma_box_elect(uint32_t dst, const CUtensorMap* m
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n\t"
         "}" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "r"(bytes)
+        : "memory");
+}
+// The same with an L2 eviction-priority hint (BWM_LAG_L2HINT == 2: pass-1 rows of the lagging
+// cursor — dates re-read h dates later as lag rows are kept, the others marked evict_first).
+__device__ __forceinline__ void tma_box_elect_hint(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                                   uint32_t bytes, bool keep) {
+    asm volatile(
+        "{\n\t.reg .pred p, k;\n\t.reg .b64 pol;\n\t"
+        "setp.ne.b32 k, %6, 0;\n\t"
+        "@k createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "@!k createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], pol;\n\t"
+        "}" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "r"(bytes), "r"((uint32_t)keep)
         : "memory");
 }
 __device__ __forceinline__ void tma_box2_elect(uint32_t dst, const CUtensorMap* map, int x, int y, int y2,
@@ -249,13 +271,13 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     const int N = prm.N, n = prm.n, h = prm.h;
     const int NA = (N + 3) & ~3;
     unsigned char* s_stage = smem_raw;                                   // [NW][S][SB]
-    // [N][SP] Z^T: fitted-value rows; for t < n they are the rows of Q (host: bwm_plan_create),
-    // so pass 1 reads its basis from the same table (full stages only touch rows < n)
-    // kRingLag (large h, C4): the tables stay in global memory and are read through L1 (uniform
-    // addresses, broadcast) so that two CTAs fit per SM next to the double-box stage rings.
+    // [N][SP] window-sum table: rows t < n are the rows of Q (pass 1), rows t >= n the window
+    // sums S_t of the fitted-value rows (pass 3) — host: bwm_plan_create
+    // kRingLag (long series): the table stays in global memory and is read through L1 (uniform
+    // addresses, broadcast).
     constexpr bool kTblSmem = MODE != kRingLag;
     float* s_tbl = reinterpret_cast<float*>(smem_raw + tma_stage_region(MODE, S));
-    const float* s_xt = kTblSmem ? s_tbl : prm.xt;
+    const float* s_xt = kTblSmem ? s_tbl : prm.wt;
     const float* s_mt = s_xt;
     float* s_bd = s_tbl + (kTblSmem ? N * SP : 0);                       // [NA] bound by row t (t >= n)
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);           // [NW][S] (SHB: [S])
@@ -264,17 +286,15 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     int* s_rows = reinterpret_cast<int*>(s_tmem + 4);                   // [tile_stages] stage -> first date
 
     if (kTblSmem)
-        for (int i = threadIdx.x; i < N * SP; i += NT) s_tbl[i] = prm.xt[i];
+        for (int i = threadIdx.x; i < N * SP; i += NT) s_tbl[i] = prm.wt[i];
     for (int i = threadIdx.x; i < N - n; i += NT) s_bd[n + i] = prm.bound[i];
     {
-        // the per-tile stage schedule (identical for every tile): pass 1 [0, n), pass 2 [w0, n)
-        // (lagging-cursor mode only), pass 3 [8 floor(n/8), N), R dates per stage
-        const int w0_ = ((n - h + 1) / kStageRows) * kStageRows, t3_ = (n / kStageRows) * kStageRows;
+        // the per-tile stage schedule (identical for every tile): pass 1 [0, n), pass 3
+        // [8 floor(n/8), N), R dates per stage
+        const int t3_ = (n / kStageRows) * kStageRows;
         const int a = (n + kStageRows - 1) / kStageRows;
-        const int b = a + (MODE == kRingTmem ? 0 : (n - w0_ + kStageRows - 1) / kStageRows);
-        const int c = b + (N - t3_ + kStageRows - 1) / kStageRows;
-        for (int i = threadIdx.x; i < c; i += NT)
-            s_rows[i] = i < a ? i * kStageRows : i < b ? w0_ + (i - a) * kStageRows : t3_ + (i - b) * kStageRows;
+        const int c = a + (N - t3_ + kStageRows - 1) / kStageRows;
+        for (int i = threadIdx.x; i < c; i += NT) s_rows[i] = i < a ? i * kStageRows : t3_ + (i - a) * kStageRows;
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < tma_barriers(MODE, S); ++s) mbar_init(s_bar + s, 1);
@@ -290,8 +310,10 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     const int64_t n_tiles = prm.n_pixels / TILE;       // host guarantees whole tiles
     const int64_t ld = prm.ld_y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wstart = n - h + 1;                      // first row of MOSUM window 0 (mosum.py:59)
-    const int w0 = (wstart / R) * R;                   // first row of the (aligned) pass-2 stream
+    // initial window: dates [n-h, n) (window 0 of mosum.py:59 is [n-h+1, n]; the first
+    // monitoring step adds date n and drops date n-h like every later one)
+    const int wstart = n - h;
+    const int w0 = (wstart / R) * R;                   // first parked row (TMEM ring)
     const int t3 = (n / R) * R;                        // first row of the (aligned) monitoring stream
     const int tid = threadIdx.x;
     const int wu = __shfl_sync(0xffffffffu, warp, 0);              // warp index, known warp-uniform
@@ -304,9 +326,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     // re-arming a slot is a lookup.  The slot being re-armed was read by this warp through
     // the generic proxy; __syncwarp() in release() orders those reads before lane 0 issues
     // the copy (the same release->acquire ordering an mbarrier handshake gives a producer).
-    // TMEM mode has no pass-2 stages: pass 1 parks the filled window-0 dates in the ring
-    const int st1 = (n + R - 1) / R, st2 = MODE == kRingTmem ? 0 : (n - w0 + R - 1) / R;
-    const int tile_stages = st1 + st2 + (N - t3 + R - 1) / R;
+    const int st1 = (n + R - 1) / R;
+    const int tile_stages = st1 + (N - t3 + R - 1) / R;
     // The slot re-armed at a release is the one just consumed, so the issue cursor needs only
     // (tile, stage); the first date of a stage comes from the schedule table.
     int64_t itile = blockIdx.x;
@@ -318,8 +339,10 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         if (really) {
             const int r0 = s_rows[istage];
             const uint32_t dst = stage_u32 + (uint32_t)(slot * SBX), bar = bar_u32 + (uint32_t)(slot * 8);
-            if (kLag && istage >= st1 + st2)
-                tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBox, kBox);   // + dates t-h (<0: zero fill)
+            if (kLag && istage >= st1)
+                tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBox, kBox);   // + dates t-h
+            else if (kLag && BWM_LAG_L2HINT == 2)
+                tma_box_elect_hint(dst, &prm.tmap, xw, r0, bar, kBox, r0 + R > n - h);
             else
                 tma_box_elect(dst, &prm.tmap, xw, r0, bar, kBox);
         }
@@ -337,9 +360,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     auto tcol = [&](int row) -> uint32_t { return tbase + (uint32_t)(2 * row); };
     // ring row q of time t is t mod L (2 columns per row: 2L columns, no mirror rows)
     // ring rows of the fixed dates of every tile (one modulo each, per CTA)
-    const int q_w0 = MODE == kRingTmem ? w0 % L : 0, q_wstart = MODE == kRingTmem ? wstart % L : 0;
+    const int q_w0 = MODE == kRingTmem ? w0 % L : 0;
     const int q_t3 = MODE == kRingTmem ? t3 % L : 0, q_t3h = MODE == kRingTmem ? ((t3 - h) % L + L) % L : 0;
-    const int q_nh = MODE == kRingTmem ? (n - h) % L : 0;
     auto ring_put_row = [&](int q, float2 v) {                             // q < L (+ mirror)
         tmem_st2(tcol(q), v);
         if (kMirror && q < R) tmem_st2(tcol(q + L), v);
@@ -412,11 +434,12 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         float2 hi[NP], lo[NP], part[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) { hi[i] = lo[i] = part[i] = f2(0.f, 0.f); }
-        float2 qpart = f2(0.f, 0.f);
-        double q0 = 0.0, q1 = 0.0;
+        float2 qpart = f2(0.f, 0.f), wpart = f2(0.f, 0.f);
+        double q0 = 0.0, q1 = 0.0, wd0 = 0.0, wd1 = 0.0;   // ||y-c||^2, window sum of [n-h, n)
         float2 c = f2(0.f, 0.f);
         bool f0 = false, f1 = false;
-        float2 last = f2(0.f, 0.f), lastw = f2(0.f, 0.f);
+        float2 last = f2(0.f, 0.f);
+        float2 lag_last = f2(0.f, 0.f);                   // LAG: fill state before date n-h
         float2 negc = f2(0.f, 0.f);
         int pr = q_w0;                                    // ring row of the next parked stage
         for (int t0 = 0; t0 < n; t0 += R) {
@@ -439,10 +462,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
                 }
                 negc = f2(-c.x, -c.y);
             }
-            // rows >= n of the last stage: zero mapping rows (exact no-ops) and no q update; the
-            // fill state they leave behind is reset before pass 2
             // TMEM mode: the filled values of the dates [w0, n) also go to their ring rows
-            // (t mod L); they become the window-0 residuals once beta is known (no re-read)
+            // (t mod L) — the y~_{t-h} of the first monitoring dates (no re-read)
             const bool park = MODE == kRingTmem && t0 >= w0;
             if (t0 + R <= n) {
                 const float* mrow = s_mt + t0 * SP;
@@ -455,6 +476,16 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
                     qpart = fma2(vc, vc, qpart);
                 }
                 if (park) ring_store(pr, yy);
+                if (t0 + R >= wstart) {                     // stages of the initial window (and the date before it)
+#pragma unroll
+                    for (int k = 0; k < R; ++k)
+                        if (t0 + k >= wstart) wpart = add2(wpart, yy[k]);
+                    if (kLag && t0 < wstart) {              // fill state before date n-h
+#pragma unroll
+                        for (int k = 0; k < R; ++k)
+                            if (t0 + k == wstart - 1) lag_last = yy[k];
+                    }
+                }
             } else {                                            // last stage: dates [t0, n) only
 #pragma unroll 1
                 for (int k = 0; k < n - t0; ++k) {
@@ -462,17 +493,20 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
                     if (park) ring_put_row(pr + k >= L ? pr + k - L : pr + k, vc);
                     axpy_row<NP, SP>(part, vc, s_mt + (t0 + k) * SP);
                     qpart = fma2(vc, vc, qpart);
+                    if (t0 + k >= wstart) wpart = add2(wpart, vc);
+                    if (kLag && t0 + k == wstart - 1) lag_last = vc;
                 }
             }
             release();
-            if (t0 + R == w0) lastw = last;                 // fill state entering pass 2
             if (park) { pr += R; if (pr >= L) pr -= L; }
             if (((t0 + R) & (kComp - 1)) == 0 || t0 + R >= n) {
 #pragma unroll
                 for (int i = 0; i < NP; ++i) { two_sum(hi[i], lo[i], part[i]); part[i] = f2(0.f, 0.f); }
                 q0 += (double)qpart.x;
                 q1 += (double)qpart.y;
-                qpart = f2(0.f, 0.f);
+                wd0 += (double)wpart.x;
+                wd1 += (double)wpart.y;
+                qpart = wpart = f2(0.f, 0.f);
             }
         }
         const bool valid0 = f0, valid1 = f1;
@@ -492,61 +526,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         if (z0 || z1) atomicMin(prm.zero_sigma, (unsigned long long)(prm.pixel_offset + px0 + (z0 ? 0 : 1)));
         const float2 sc = sigma_scale(ss, prm.inv_dof, prm.sqrt_n, valid0, valid1);
 
-        // ---- window 0 ------------------------------------------------------------------
-        float2 acc = f2(0.f, 0.f);
-        float2 lag_last = w0 == wstart ? lastw : f2(0.f, 0.f);   // kRingLag: fill state at wstart-1
-        if (MODE == kRingTmem) {
-            // The ring rows of the dates [wstart, n) (row = date mod L, written in pass 1; h - 1
-            // < L rows, so none was overwritten) hold the filled values: convert them in place to
-            // the residuals r = y - z^T beta_Q, summing window 0 in date order — the arithmetic
-            // of a re-read pass, without re-reading.  R rows per batch, one .x2 access per row.
-            tmem_wait_st();
-            int q = q_wstart;
-#pragma unroll 1
-            for (int t0 = wstart; t0 < n; t0 += R) {
-                float2 v[R];
-                int qk[R];
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    qk[k] = q + k >= L ? q + k - L : q + k;
-                    if (t0 + k < n) ring_ld2(qk[k], v[k]);
-                }
-                tmem_wait_ld();
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    if (t0 + k < n) {
-                        const float2 r = dot_row<NP, SP>(v[k], s_xt + (t0 + k) * SP, nb);
-                        acc = add2(acc, r);
-                        ring_put_row(qk[k], r);
-                    }
-                }
-                q = q + R >= L ? q + R - L : q + R;
-            }
-        }
-        if (kLag) last = lastw;                                 // pass 2 re-reads [w0, n)
-        for (int t0 = w0; kLag && t0 < n; t0 += R) {
-            const float2* st = acquire();
-            if (t0 + R <= n) {
-                const float* xrow = s_xt + t0 * SP;
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const int t = t0 + k;
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), xrow + k * SP, nb);
-                    if (t >= wstart) acc = add2(acc, r);
-                    if (t == wstart - 1) lag_last = last;
-                }
-            } else {                                            // last stage: dates [t0, n) only
-#pragma unroll 1
-                for (int k = 0; k < n - t0; ++k) {
-                    const int t = t0 + k;
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                    if (t >= wstart) acc = add2(acc, r);
-                    if (t == wstart - 1) lag_last = last;
-                }
-            }
-            release();
-        }
-        if (MODE == kRingTmem) ring_put_row(q_nh, f2(0.f, 0.f));  // r_{n-h} is not in window 0
+        // initial window sum minus the intercept part of S^T beta_Q (float64, bwm_common.cuh)
+        float2 acc = wsum_init(wd0, wd1, hi[0], lo[0], prm.s0);
 
         // ---- pass 3: monitoring period, fused MOSUM + detect (unscaled frame) ----------
         float2 mx = f2(0.f, 0.f), msum = f2(0.f, 0.f), sr = f2(0.f, 0.f);
@@ -555,10 +536,12 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         const bool want_sup = prm.sup != nullptr;
         const float2 inv = inv_scale(sc);
         const float2 bsc = mul2(sc, f2(s_bd[n], s_bd[n]));   // LEAN: the constant boundary, unscaled
+        // one monitoring date: y~_t in, y~_{t-h} out, numerator acc - S_t^T beta_Q
         auto step = [&](const float2 r, const float2 old, const int t, const float bj) {
             acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
+            const float2 num = wsum_row<NP, SP>(acc, s_xt + t * SP, nb);
             const float2 bs = LEAN ? bsc : mul2(sc, f2(bj, bj));   // boundary in the unscaled frame
-            const float a0 = fabsf(acc.x), a1 = fabsf(acc.y);
+            const float a0 = fabsf(num.x), a1 = fabsf(num.y);
             mx.x = fmaxf(mx.x, a0);
             mx.y = fmaxf(mx.y, a1);
             const int j1 = t - n + 1;
@@ -569,8 +552,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
                     sr.x = fmaxf(sr.x, __fdividef(a0, bj));
                     sr.y = fmaxf(sr.y, __fdividef(a1, bj));
                 }
-                msum = add2(msum, acc);
-                if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)(t - n) * prm.ld_out + px0) = mul2(acc, inv);
+                msum = add2(msum, num);
+                if (mo_out) *reinterpret_cast<float2*>(mo_out + (int64_t)(t - n) * prm.ld_out + px0) = mul2(num, inv);
             }
         };
         int wb = q_t3;                                   // ring row of t0
@@ -578,7 +561,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
             const float2* lst = st + kBox / 8;           // lag dates (kRingLag): second box
-            if (t0 >= n + (kLag ? 1 : 0) && t0 + R <= N) {
+            if (t0 >= n && t0 + R <= N) {
                 float2 oldv[R], newv[R];
                 if (MODE == kRingTmem) ring_load(rb, oldv);
                 float4 b4[R / 4];
@@ -586,25 +569,26 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
                 for (int q = 0; q < R / 4; ++q)
                     b4[q] = LEAN ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(s_bd + t0)[q];
                 const float* xrow = s_xt + t0 * SP;
-                float2 acck[R];                          // LEAN: window sums of the stage
+                float2 acck[R];                          // LEAN: MOSUM numerators of the stage
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const int t = t0 + k;
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), xrow + k * SP, nb);
+                    const float2 r = fill(st[k * ROWF2], negc, last);
                     float2 old;
                     if (MODE == kRingTmem) {
                         old = oldv[k];
                         newv[k] = r;
                     } else {
-                        old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), xrow + (k - h) * SP, nb);
+                        old = fill(lst[k * ROWF2], negc, lag_last);
                     }
                     if (LEAN && BWM_LAZY_CROSS) {
                         // constant boundary: the first crossing is the first date whose running max
                         // exceeds it, so the per-date test moves out of the loop (below)
                         acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
-                        acck[k] = acc;
-                        mx.x = fmaxf(mx.x, fabsf(acc.x));
-                        mx.y = fmaxf(mx.y, fabsf(acc.y));
+                        const float2 num = wsum_row<NP, SP>(acc, xrow + k * SP, nb);
+                        acck[k] = num;
+                        mx.x = fmaxf(mx.x, fabsf(num.x));
+                        mx.y = fmaxf(mx.y, fabsf(num.y));
                     } else {
                         const float4 bq4 = b4[k >> 2];
                         step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
@@ -632,13 +616,13 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
 #pragma unroll 1
                 for (int k = k0; k < k1; ++k) {
                     const int t = t0 + k;
-                    const float2 r = dot_row<NP, SP>(fill(st[k * ROWF2], negc, last), s_xt + t * SP, nb);
-                    float2 old = f2(0.f, 0.f);
+                    const float2 r = fill(st[k * ROWF2], negc, last);
+                    float2 old;
                     if (MODE == kRingTmem) {
                         old = ring_get_row(rb + k);
                         ring_put_row(wb + k, r);
-                    } else if (t > n) {                        // r_{n-h} is outside window 0
-                        old = dot_row<NP, SP>(fill(lst[k * ROWF2], negc, lag_last), s_xt + (t - h) * SP, nb);
+                    } else {
+                        old = fill(lst[k * ROWF2], negc, lag_last);
                     }
                     step(r, old, t, s_bd[t]);
                 }

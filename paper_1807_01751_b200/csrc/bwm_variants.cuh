@@ -36,10 +36,15 @@ constexpr int kTmaLean = 0x10;   // pick(): OR into the TMA ring mode for the LE
 
 // Defines bwm::KernelFn bwm_pick_mma_p<NP>(int lean): the lagging-cursor kernel with the
 // fitted values on the tensor cores (bwm_kernel_mma.cuh).
+#if BWM_STAGE_ROWS == 8
 #define BWM_DEFINE_PICK_MMA(NP)                                                                  \
     bwm::KernelFn bwm_pick_mma_p##NP(int lean) {                                                 \
         return lean ? bwm::monitor_kernel_mma<NP, true> : bwm::monitor_kernel_mma<NP, false>;   \
     }
+#else   // experimental 16-date stages: no tensor-core variant
+#define BWM_DEFINE_PICK_MMA(NP) \
+    bwm::KernelFn bwm_pick_mma_p##NP(int) { return nullptr; }
+#endif
 
 // Defines bwm::KernelFn bwm_pick_masked_p<NP>(int big, int keep): the masked-NaN kernel with
 // its residual rings in shared memory (big = 0) or global memory (big = 1), writing the MOSUM
