@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BWM_ABI_VERSION 6
+#define BWM_ABI_VERSION 7
 
 /* error codes (negative); positive returns are cudaError_t values */
 #define BWM_OK 0
@@ -223,6 +223,17 @@ int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info);
 /* Stream-ordered reset of a device zero_sigma_pixel slot to INT64_MAX (two cudaMemsetAsync,
    no kernel, no allocation): lets a caller reuse one slot across bwm_monitor calls. */
 int bwm_zero_sigma_init(int64_t* zero_sigma_pixel_device, void* stream);
+
+/*
+ * The null-hypothesis draws of critical_value on the device (reference mosum.py:195-198:
+ * replication r draws np.random.Generator(np.random.Philox(key=seed, counter=r << 128))
+ * .standard_normal(n_obs)).  numpy's Philox4x64-10 + ziggurat restated bit for bit; the draws of
+ * replications [rep0, rep0 + reps) are written as float32 to out[t * ld + (r - rep0)]
+ * (time-major, one column per replication: a stack bwm_monitor takes directly).  seed = seed_lo +
+ * 2^64 seed_hi.  Asynchronous on `stream`.
+ */
+int bwm_null_draws(uint64_t seed_lo, uint64_t seed_hi, int64_t rep0, int64_t reps, int32_t n_obs,
+                   float* out, int64_t ld, void* stream);
 
 /* Number of bwm kernel launches issued by this process so far (all plans). */
 int64_t bwm_launch_count(void);

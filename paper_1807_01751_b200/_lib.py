@@ -27,7 +27,7 @@ BWM_NAN_MASK = 1
 NAN_MODES = {"fill": BWM_NAN_FILL, "mask": BWM_NAN_MASK}
 
 INT64_MAX = (1 << 63) - 1
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 
 class Dims(C.Structure):
@@ -96,6 +96,8 @@ SIGNATURES = [
      [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("bwm_plan_info", C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
     ("bwm_zero_sigma_init", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("bwm_null_draws", C.c_int,
+     [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
     ("bwm_launch_count", C.c_int64, []),
     ("bwm_smem_bytes", C.c_int64, [C.POINTER(Dims)]),
     ("bwm_last_error", C.c_char_p, []),

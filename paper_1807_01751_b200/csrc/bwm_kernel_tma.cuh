@@ -73,7 +73,8 @@ constexpr bool kMirror = BWM_RING_MIRROR != 0;
 #define BWM_SHARED_BOX 0   // 1: one CTA-wide 256-px box per stage (1 KB rows), re-armed by the last warp to release it
 #endif
 #ifndef BWM_LAGT_WARPS
-#define BWM_LAGT_WARPS 4   // warps per CTA of the lagging-cursor kernel with smem tables (tables shared by all)
+#define BWM_LAGT_WARPS 16  // warps per CTA of the lagging-cursor kernel with smem tables (tables shared by all;
+                           // C4: 16 warps x 2 stages at 1 CTA/SM 5.27 ms, 8 warps 5.87 (3 stages), 4 warps x 2 CTAs 6.09)
 #endif
 // the lagging-cursor mode moves two boxes per stage (dates t and t-h): 3 stages = 6 boxes
 // (kRingLag: tables in global memory, 3 stages, 3 CTAs/SM; kRingLagT: tables in smem, 2 stages,

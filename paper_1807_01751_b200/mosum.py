@@ -2,11 +2,13 @@
 
 ``log_plus`` and ``boundary_values`` are the per-geometry constants the kernel compares
 against (mosum.py:27-32, 68-79).  ``critical_value`` is the Monte Carlo calibration of
-lambda (mosum.py:166-227): the null draws come from the same per-replication Philox
-substreams as the reference, and ALL replications run as one stack through the same fused
-GPU kernel as the data (libbwm), which emits the per-replication statistic
-sup_j |MO_j| / sqrt(log_plus) directly (bwm_outputs.sup_stat) — no MOSUM matrix, no CPU
-MOSUM in this package.
+lambda (mosum.py:166-227), entirely on the device: libbwm draws every replication's null
+series from the reference's own per-replication Philox substreams (bwm_null_draws: numpy's
+Philox4x64-10 + ziggurat restated bit for bit, one thread per replication, straight into a
+time-major stack), and ALL replications run as one stack through the same fused kernel as the
+data, which emits the per-replication statistic sup_j |MO_j| / sqrt(log_plus) directly
+(bwm_outputs.sup_stat) — no host draws, no MOSUM matrix, no CPU MOSUM in this package.
+``null_draws`` is the host restatement of the same streams (numpy), kept for the checks.
 """
 
 from __future__ import annotations
@@ -113,17 +115,20 @@ def critical_value(request: CriticalValueRequest, threads: int = 1, device=None)
 
     Same geometry rules as the reference (mosum.py:166-227): regular axis 1..N with
     N = round(horizon * n_sim), h = round(h_frac * n_sim), the full season-trend fit per
-    replication.  The draws (host, the reference's Philox substreams, `threads` workers)
-    fill one float32 stack of all replications; one libbwm launch over it emits each
-    replication's statistic (sup_stat), so the statistic sees float32 residual arithmetic:
-    agreement with the float64 reference is ~1e-6 relative, not bit-exact.
+    replication.  The draws are the reference's (bit-identical Philox substreams), generated
+    on the device in float32 — the dtype the monitor kernel reads; one libbwm launch over all
+    replications emits each one's statistic (sup_stat), so the statistic sees float32 residual
+    arithmetic: agreement with the float64 reference is ~1e-6 relative, not bit-exact.
+    `threads` is accepted for the reference signature and unused (no host work).
     """
-    from concurrent.futures import ThreadPoolExecutor
-
-    from .device import DevicePlan
+    import ctypes as C
 
     import torch
 
+    from . import _lib
+    from .device import DevicePlan
+
+    del threads
     n_hist = request.n_sim
     n_obs = int(round(request.horizon * n_hist))
     bandwidth = int(round(request.h_frac * n_hist))
@@ -136,15 +141,13 @@ def critical_value(request: CriticalValueRequest, threads: int = 1, device=None)
     axis = regular_axis(n_obs)
     # unit lambda: bound_j = sqrt(log_plus((n+1+j)/n)), so sup_stat is the reference statistic
     plan = DevicePlan.get(axis, request.freq, request.harmonics, n_hist, bandwidth, 1.0, device)
-    blocks = [(s, min(s + REPLICATION_BLOCK, request.reps)) for s in range(0, request.reps, REPLICATION_BLOCK)]
-    host = torch.empty((n_obs, request.reps), dtype=torch.float32, pin_memory=True).numpy()
-
-    def draws(block):
-        null_draws(request, block[0], block[1], n_obs, out=host[:, block[0]:block[1]])
-
-    with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
-        list(pool.map(draws, blocks))
-    y = torch.as_tensor(host).to(plan.torch_device, non_blocking=True)
+    dev = plan.torch_device
+    y = torch.empty((n_obs, request.reps), dtype=torch.float32, device=dev)
+    seed = int(request.seed)
+    with torch.cuda.device(dev):
+        stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        _lib.check(plan._lib.bwm_null_draws(seed & ((1 << 64) - 1), seed >> 64, 0, request.reps, n_obs,
+                                            y.data_ptr(), request.reps, stream), "bwm_null_draws")
     res = plan.run_device(y, sup=True)
     if res.zero_sigma is not None:
         from .errors import ZeroResidualError

@@ -249,6 +249,31 @@ def test_critical_value_matches_pinned():
     assert lam == pytest.approx(pinned["value"], rel=2e-5)
 
 
+@pytest.mark.parametrize("seed,rep0,reps,n_obs", [(1, 0, 2048, 200), (7, 49000, 1000, 228), (2**64 - 5, 3, 300, 1000)])
+def test_null_draws_match_numpy(seed, rep0, reps, n_obs):
+    """bwm_null_draws (device Philox4x64-10 + ziggurat) reproduces the reference's null series
+    bit for bit: replication r = Generator(Philox(key=seed, counter=r << 128)).standard_normal
+    (reference mosum.py:195-198), as float32.  The samples cover ziggurat wedge and tail draws
+    (~0.7% of draws leave the fast path)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1807_01751_b200 import _lib
+    from paper_1807_01751_b200.mosum import CriticalValueRequest, null_draws
+
+    lib = _lib.load()
+    ld = reps + 5                                  # padded leading dimension
+    out = torch.full((n_obs, ld), float("nan"), dtype=torch.float32, device="cuda")
+    _lib.check(lib.bwm_null_draws(seed & ((1 << 64) - 1), seed >> 64, rep0, reps, n_obs, out.data_ptr(), ld,
+                                  C.c_void_p(torch.cuda.current_stream().cuda_stream)), "bwm_null_draws")
+    req = CriticalValueRequest(alpha=0.05, h_frac=0.5, horizon=2.0, n_sim=100, reps=1000, seed=seed)
+    ref = null_draws(req, rep0, rep0 + reps, n_obs, dtype=np.float32)
+    got = out.cpu().numpy()
+    assert np.array_equal(got[:, :reps].view(np.uint32), ref.view(np.uint32))
+    assert np.isnan(got[:, reps:]).all()          # nothing written past the replications
+
+
 @pytest.mark.parametrize("N,n,h,k", [(3000, 1500, 20, 8), (2600, 1300, 400, 6)])
 def test_long_series(N, n, h, k):
     """Series too long for shared-memory tables (N * p floats > 227 KB): the lagging-cursor
