@@ -57,7 +57,12 @@ namespace bwm {
 constexpr int kStageRows = BWM_STAGE_ROWS;      // dates per stage (multiple of 8)
 #ifndef BWM_LAG_L2HINT
 #define BWM_LAG_L2HINT 0   // L2 evict_last/evict_first hints on the lag boxes: measured 8.21 vs 8.18 ms at C4, off
+#endif                     // 2: also pass-1 rows and never-re-read lead rows (evict_first)
+#ifndef BWM_LAG_KEEP
+#define BWM_LAG_KEEP 1.0   // fraction of a kept box's lines that get evict_last (createpolicy.fractional)
 #endif
+#define BWM_STR2(x) #x
+#define BWM_STR(x) BWM_STR2(x)
 #ifndef BWM_STAGES_LAG
 #define BWM_STAGES_LAG 3
 #endif
@@ -145,7 +150,7 @@ __device__ __forceinline__ void tma_box_elect_hint(uint32_t dst, const CUtensorM
     asm volatile(
         "{\n\t.reg .pred p, k;\n\t.reg .b64 pol;\n\t"
         "setp.ne.b32 k, %6, 0;\n\t"
-        "@k createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "@k createpolicy.fractional.L2::evict_last.b64 pol, " BWM_STR(BWM_LAG_KEEP) ";\n\t"
         "@!k createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
         "elect.sync _|p, 0xffffffff;\n\t"
         "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%4], %5;\n\t"
@@ -155,17 +160,20 @@ __device__ __forceinline__ void tma_box_elect_hint(uint32_t dst, const CUtensorM
         : "memory");
 }
 __device__ __forceinline__ void tma_box2_elect(uint32_t dst, const CUtensorMap* map, int x, int y, int y2,
-                                               uint32_t bar, uint32_t bytes, uint32_t box_bytes = kBoxBytes) {
+                                               uint32_t bar, uint32_t bytes, uint32_t box_bytes = kBoxBytes,
+                                               bool keep_lead = true) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, kl;\n\t"
         "elect.sync _|p, 0xffffffff;\n\t"
         "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%5], %6;\n\t"
 #if BWM_LAG_L2HINT
         // dates t: re-read h dates later as the lag box -> keep in L2; dates t-h: last use
-        ".reg .b64 keep, drop;\n\t"
-        "createpolicy.fractional.L2::evict_last.b64 keep, 1.0;\n\t"
+        ".reg .b64 keep, drop, lead;\n\t"
+        "setp.ne.b32 kl, %8, 0;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 keep, " BWM_STR(BWM_LAG_KEEP) ";\n\t"
         "createpolicy.fractional.L2::evict_first.b64 drop, 1.0;\n\t"
-        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%2, {%3, %4}], [%5], keep;\n\t"
+        "selp.b64 lead, keep, drop, kl;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%2, {%3, %4}], [%5], lead;\n\t"
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%1], [%2, {%3, %7}], [%5], drop;\n\t"
 #else
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%2, {%3, %4}], [%5];\n\t"
@@ -173,7 +181,7 @@ __device__ __forceinline__ void tma_box2_elect(uint32_t dst, const CUtensorMap* 
 #endif
         "}" ::"r"(dst),
         "r"(dst + box_bytes), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
-        "r"(bar), "r"(bytes), "r"(y2)
+        "r"(bar), "r"(bytes), "r"(y2), "r"((uint32_t)keep_lead)
         : "memory");
 }
 
@@ -341,7 +349,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
             const int r0 = s_rows[istage];
             const uint32_t dst = stage_u32 + (uint32_t)(slot * SBX), bar = bar_u32 + (uint32_t)(slot * 8);
             if (kLag && istage >= st1)
-                tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBox, kBox);   // + dates t-h
+                tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBox, kBox,    // + dates t-h
+                               BWM_LAG_L2HINT < 2 || r0 + R <= N - h);                  // re-read as a lag row?
             else if (kLag && BWM_LAG_L2HINT == 2)
                 tma_box_elect_hint(dst, &prm.tmap, xw, r0, bar, kBox, r0 + R > n - h);
             else
