@@ -273,7 +273,6 @@ struct bwm_plan {
     bwm_dims dims{};
     int device = 0;
     int sp = 0;
-    float* d_mt = nullptr;
     float* d_xt = nullptr;
     float* d_bound = nullptr;
     float* d_rinv = nullptr;
@@ -343,7 +342,6 @@ static int validate_dims(const bwm_dims* d) {
 }
 
 static void plan_free_tables(bwm_plan* plan) {
-    cudaFree(plan->d_mt);
     cudaFree(plan->d_xt);
     cudaFree(plan->d_bound);
     cudaFree(plan->d_rinv);
@@ -630,10 +628,8 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
             Rinv[(size_t)i * p + col] = v / Rm[(size_t)i * p + i];
         }
     // float32 tables, transposed so one date's coefficients are contiguous (LDS.128)
-    std::vector<float> mt((size_t)n * sp, 0.f), xt((size_t)N * sp, 0.f), bd((size_t)(N - n)),
-        ri((size_t)p * p);
-    for (int t = 0; t < n; ++t)
-        for (int i = 0; i < p; ++i) mt[(size_t)t * sp + i] = (float)Q[(size_t)t * p + i];
+    // (Z^T: the tensor-core fitted-value kernel, bwm_kernel_mma.cuh, reads its Q rows from it)
+    std::vector<float> xt((size_t)N * sp, 0.f), bd((size_t)(N - n)), ri((size_t)p * p);
     for (int t = 0; t < N; ++t)
         for (int i = 0; i < p; ++i) {      // z_t = R^-T x_t  <=>  z_t,i = sum_k Rinv[k][i] x_k,t
             double z = 0.0;
@@ -691,12 +687,9 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         return set_err((int)e, "%s: %s", what, cudaGetErrorString(e));
     };
     cudaError_t e;
-    if ((e = cudaMalloc(&plan->d_mt, mt.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&plan->d_xt, xt.size() * 4)) != cudaSuccess) return fail(e, "cudaMalloc");
     if ((e = cudaMalloc(&plan->d_bound, std::max<size_t>(bd.size(), 1) * 4)) != cudaSuccess)
         return fail(e, "cudaMalloc");
-    if ((e = cudaMemcpy(plan->d_mt, mt.data(), mt.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
-        return fail(e, "cudaMemcpy");
     if ((e = cudaMemcpy(plan->d_xt, xt.data(), xt.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
         return fail(e, "cudaMemcpy");
     if ((e = cudaMemcpy(plan->d_bound, bd.data(), bd.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
@@ -868,7 +861,6 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     k.n = d.n_hist;
     k.h = d.bandwidth;
     k.sp = plan->sp;
-    k.mt = plan->d_mt;
     k.xt = plan->d_xt;
     k.bound = plan->d_bound;
     k.rinv = plan->d_rinv;

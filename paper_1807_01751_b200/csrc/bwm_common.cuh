@@ -30,8 +30,7 @@ struct KParams {
     int64_t n_pixels;
     int64_t pixel_offset;       // global index of pixel 0 (zero-sigma reporting)
     int N, n, h, sp;            // sp: padded row stride of the coefficient tables
-    const float* mt;            // [n][sp]  Q^T: orthonormal history basis, row t = date t
-    const float* xt;            // [N][sp]  Z^T = (R^-T X')^T: fitted value = z_t . beta_Q
+    const float* xt;            // [N][sp]  Z^T = (R^-T X')^T (rows t < n: Q^T), the MMA kernel's table
     const float* rinv;          // [p][p]   R^-1 (row-major): beta' = R^-1 beta_Q (beta output)
     const float* bound;         // [N-n]
     float inv_dof;              // 1 / (n - p)
