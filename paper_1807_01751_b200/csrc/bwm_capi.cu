@@ -479,7 +479,7 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
                                      bwm::masked_tmem_cols(p), plan->device, &e);
     if (e != cudaSuccess) return fail(e, "cudaFuncGetAttributes");
     if (plan->mbig) {
-        const size_t rb = (size_t)plan->sms * plan->bpm_masked * bwm::masked_scratch_words(h, p) * bwm::kMaskThreads * 4;
+        const size_t rb = (size_t)plan->sms * plan->bpm_masked * bwm::masked_scratch_words(h, p, true) * bwm::kMaskThreads * 4;
         if ((e = cudaMalloc(&plan->d_ring, rb)) != cudaSuccess) return fail(e, "cudaMalloc(ring)");
     }
     *out_plan = plan;

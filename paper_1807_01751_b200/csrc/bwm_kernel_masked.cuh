@@ -23,11 +23,12 @@
 //   stream from L2 through a 3-stage shared-memory ring (cp.async.bulk).  G_v = G_full - Gm
 //   is accurate because Gm has few terms; the refinement step below absorbs the rest.
 // Solve: float32 Cholesky of G_v per pixel (in registers), beta' = G_v^-1 g.
-// Pass 2 (history again, L2): two-pass RSS of the valid dates; the last h_v - 1 valid
-//   residuals (and their dates) go to a per-pixel ring (slot 0 = 0: the element before
-//   window 0).  The same sweep accumulates the normal-equation residual e = X_v r, and one
-//   step of mixed-precision iterative refinement follows: dbeta = G_v^-1 e, RSS and the ring
-//   residuals are corrected in place (RSS' = RSS - 2 dbeta.e + |L^T dbeta|^2).  This makes
+// Pass 2 (history again, L2): two-pass RSS of the valid dates and the normal-equation
+//   residual e = X_v r; one step of mixed-precision iterative refinement follows: dbeta =
+//   G_v^-1 e, beta and RSS are corrected (RSS' = RSS - 2 dbeta.e + |L^T dbeta|^2).  A tail
+//   sweep from the warp's earliest window-0 date then puts the last h_v - 1 valid residuals,
+//   computed with the refined beta, in a per-pixel ring (slot 0 = 0: the element before
+//   window 0) — coalesced row loads instead of per-lane gathers of X' rows.  This makes
 //   the float32 Gram good to cond(G_v) ~ 1e5 (p = 18 on 23 valid dates: cond 3e4) at the cost
 //   of p/2 FFMA2 per valid history date; realistic stacks have cond(G_v) < 10.
 // Pass 3 (monitoring): per valid date r, old = ring[s], ring[s] = r, acc += r - old,
@@ -100,8 +101,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         : "memory");
 }
 
-// Per-thread scratch words: ring [h] floats + ring dates [h] uint16.
-__host__ __device__ inline int masked_scratch_words(int h, int p) { return h + (h + 1) / 2 + 0 * p; }
+// Per-thread scratch words: the residual ring [h] floats, + its dates [h] uint16 (shared-memory ring).
+__host__ __device__ inline int masked_scratch_words(int h, int p, bool big) { return big ? h + 0 * p : h + (h + 1) / 2; }
 
 // Shared-memory bytes of the masked kernel (host mirror in bwm_capi.cu).
 __host__ __device__ inline int64_t masked_smem_bytes(int N, int n, int h, int p, bool big) {
@@ -109,7 +110,7 @@ __host__ __device__ inline int64_t masked_smem_bytes(int N, int n, int h, int p,
     // X'^T with zero rows past N; in BIG mode it stays in global memory (read through L1)
     int64_t bytes = big ? 0 : (((int64_t)(N + kMaskD) * sp * 4 + 127) / 128) * 128;
     bytes += (int64_t)kMaskBStages * gram_nn(p) * 128;                      // x x^T tile ring
-    if (!big) bytes += (int64_t)masked_scratch_words(h, p) * kMaskThreads * 4;
+    if (!big) bytes += (int64_t)masked_scratch_words(h, p, false) * kMaskThreads * 4;
     return bytes + (2 * kMaskBStages + kMaskABufs) * 8 + 32;                // mbarriers + TMEM slot + tickets
 }
 
@@ -135,6 +136,14 @@ __device__ __forceinline__ void chol_col(float (&L)[NP * (NP + 1) / 2], float (&
         }
         chol_col<NP, J + 1>(L, dinv, ok);
     }
+}
+
+// b_j = lambda sqrt(log_plus(x_j)) for x_j = (n_v + 1 + j) / n_v > e (mosum.py:68-79), in the
+// unscaled frame (lam_sc = lambda sigma sqrt(n_v)); within ~1e-7 of the float64 value
+static __device__ __noinline__ float masked_bound(float lam_sc, int j, float dx, float jx0) {
+    const float x = fmaf((float)j, dx, jx0);
+    const float lp = fmaxf(__log2f(x) * 0.69314718f, 1.f);
+    return lam_sc * (lp * rsqrtf(lp));
 }
 
 // idle lanes of a tail tile read this NaN (stride 0): every date missing, no per-row test
@@ -166,7 +175,7 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
     unsigned char* s_b = smem_raw + (BIG ? 0 : (((N + D) * SP * 4 + 127) / 128) * 128);   // [S][SB] x x^T tiles
     float* s_ring = reinterpret_cast<float*>(s_b + S * SB);           // ring scratch   (!BIG)
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(s_ring) +
-                                                  (BIG ? 0 : masked_scratch_words(h, NP) * kMaskThreads * 4));
+                                                  (BIG ? 0 : masked_scratch_words(h, NP, false) * kMaskThreads * 4));
     uint64_t* b_full = s_bar;              // [S]  tile landed
     uint64_t* b_empty = s_bar + S;         // [S]  MMAs reading the tile are done
     uint64_t* m_done = s_bar + 2 * S;      // [AB] MMAs reading A buffer b are done
@@ -188,9 +197,9 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
     const uint32_t tbase = *s_tmem;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;            // this warp's TMEM lane quarter
     const uint32_t d_col = tbase, a_col = tbase + NN;                 // Gm accumulator | AB x 16 A columns
-    float* ring = (BIG ? prm.ring_g + (int64_t)blockIdx.x * masked_scratch_words(h, NP) * kMaskThreads : s_ring) +
+    float* ring = (BIG ? prm.ring_g + (int64_t)blockIdx.x * masked_scratch_words(h, NP, true) * kMaskThreads : s_ring) +
                   tid;
-    uint16_t* ring_d = reinterpret_cast<uint16_t*>(ring - tid + h * kMaskThreads) + tid;   // ring dates
+    uint16_t* ring_d = reinterpret_cast<uint16_t*>(ring - tid + h * kMaskThreads) + tid;   // ring dates (!BIG)
 
     const int64_t ld = prm.ld_y;
     const float lam = prm.lambda;
@@ -369,17 +378,17 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
             return r2.x + r2.y;
         };
 
-        // ---- pass 2: RSS (two-pass) and the history part of window 0 -----------------------
+        // ---- pass 2: RSS (two-pass) and the refinement residual e = X_v r --------------------
         const int hv = (int)(((int64_t)h * nv) / n);
         const int wfirst = nv - hv + 1;          // 0-based compacted index of window 0's first element
-        // branch-free bodies: per-pixel state advances by selects, ring writes are predicated
         constexpr int RS = kMaskThreads;         // ring row stride (words)
-        int seen = 0, so = RS;                   // so: word offset of the next ring slot (slot 1)
+        int seen = 0, tw = n;                    // tw: date of compacted index wfirst (window 0 start)
+        int so = RS;                             // word offset of the next ring slot (slot 1)
+        if (hv >= 1) ring[0] = 0.f;              // the element before window 0
         double rss = 0.0;
         float2 e2[NP / 2];                       // X_v r (normal-equation residual)
 #pragma unroll
         for (int i = 0; i < NP / 2; ++i) e2[i] = f2(0.f, 0.f);
-        if (hv >= 1) ring[0] = 0.f;              // the element before window 0
         for (int t0 = 0; t0 < n; t0 += D23) {
             float vb[D23];
             load(t0, n, vb);
@@ -398,19 +407,22 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
                     if (4 * q + 1 < NP) e2[2 * q] = fma2(f2(rm, rm), f2(x.x, x.y), e2[2 * q]);
                     if (4 * q + 3 < NP) e2[2 * q + 1] = fma2(f2(rm, rm), f2(x.z, x.w), e2[2 * q + 1]);
                 }
-                const bool inwin = m && seen >= wfirst;
-                if (inwin) {
-                    ring[so] = r;
-                    ring_d[so] = (uint16_t)t;
+                if (BIG) {
+                    tw = (m && seen == wfirst) ? t : tw;
+                } else {                         // shared-memory ring: window 0 written here
+                    const bool inwin = m && seen >= wfirst;
+                    if (inwin) {
+                        ring[so] = r;
+                        ring_d[so] = (uint16_t)t;
+                    }
+                    so += inwin ? RS : 0;
                 }
-                so += inwin ? RS : 0;
                 seen += m ? 1 : 0;
             }
             rss += (double)part;
         }
-        const int slot = so / RS;
 
-        // ---- one refinement step: dbeta = G_v^-1 e; correct RSS and the window residuals ---
+        // ---- one refinement step: dbeta = G_v^-1 e; correct RSS and beta ----------------------
         float db[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) db[i] = (i & 1) ? e2[i >> 1].y : e2[i >> 1].x;
@@ -435,20 +447,62 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
         double de = 0.0;
 #pragma unroll
         for (int i = 0; i < NP; ++i) de += (double)db[i] * (double)((i & 1) ? e2[i >> 1].y : e2[i >> 1].x);
+        float2 nb0[NP / 2];                      // pre-refinement -beta' (window-0 residuals, BIG)
+#pragma unroll
+        for (int i = 0; i < NP / 2; ++i) nb0[i] = nb[i];
         if (ok) {
             rss = fmax(rss - 2.0 * de + quad, 0.0);
 #pragma unroll
             for (int i = 0; i < NP / 2; ++i) nb[i] = sub2(nb[i], f2(db[2 * i], db[2 * i + 1]));
         }
+
+        // ---- window 0: the last hv - 1 valid history residuals, corrected by the refinement ---
+        // r = r(beta_0) - dbeta . x_t, the same arithmetic either way.  Shared-memory ring: the
+        // pass-2 residuals are corrected in place from the stored dates.  Global ring (BIG): a
+        // tail sweep from the warp's earliest window-0 date recomputes them — coalesced row loads
+        // and one X' row per date for the warp, instead of per-lane gathers of X' rows from
+        // global memory and a per-element date ring.
         float acc = 0.f;
-        for (int s2 = 1; s2 < slot; ++s2) {
-            const int t = ring_d[s2 * kMaskThreads];
-            const float* xr = s_x + t * SP;
-            float r = ring[s2 * kMaskThreads];
+        if (!BIG) {
+            const int slot = so / RS;
+            for (int s2 = 1; s2 < slot; ++s2) {
+                const int t = ring_d[s2 * kMaskThreads];
+                const float* xr = s_x + t * SP;
+                float r = ring[s2 * kMaskThreads];
 #pragma unroll
-            for (int i = 0; i < NP; ++i) r = fmaf(-db[i], xr[i], r);
-            ring[s2 * kMaskThreads] = r;
-            acc += r;
+                for (int i = 0; i < NP; ++i) r = fmaf(-db[i], xr[i], r);
+                ring[s2 * kMaskThreads] = r;
+                acc += r;
+            }
+        } else {
+            int tlo = tw;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tlo = min(tlo, __shfl_xor_sync(0xffffffffu, tlo, o));
+            for (int t0 = tlo; t0 < n; t0 += D23) {
+                float vb[D23];
+                load(t0, n, vb);
+#pragma unroll
+                for (int k = 0; k < D23; ++k) {
+                    const int t = t0 + k;
+                    const bool inwin = finitef(vb[k]) && t >= tw && t < n;
+                    const float yc = inwin ? vb[k] - c : 0.f;
+                    float2 r2 = f2(yc, 0.f);                         // resid() with beta_0
+                    const float* xr = s_x + t * SP;
+                    const float4* x4 = reinterpret_cast<const float4*>(xr);
+#pragma unroll
+                    for (int q = 0; q < SP / 4; ++q) {
+                        const float4 x = x4[q];
+                        if (4 * q + 1 < NP) r2 = fma2(nb0[2 * q], f2(x.x, x.y), r2);
+                        if (4 * q + 3 < NP) r2 = fma2(nb0[2 * q + 1], f2(x.z, x.w), r2);
+                    }
+                    float r = r2.x + r2.y;
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) r = fmaf(-db[i], xr[i], r);
+                    if (inwin) ring[so] = r;
+                    so += inwin ? RS : 0;
+                    acc += inwin ? r : 0.f;
+                }
+            }
         }
         const float ss = ok ? (float)rss : 0.f;
         const bool fit_ok = ok && hv >= 1;
@@ -472,7 +526,6 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
         for (int t0 = n; t0 < N; t0 += D23) {
             float vb[D23];
             load(t0, N, vb);
-            const bool slow = __any_sync(0xffffffffu, j + D23 > je);   // warp-uniform
 #pragma unroll
             for (int k = 0; k < D23; ++k) {
                 const int t = t0 + k;
@@ -483,17 +536,15 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
                 const int ro1 = ro + RS == ro_end ? 0 : ro + RS;
                 ro = m ? ro1 : ro;
                 acc = m ? acc + (r - old) : acc;
-                // b_j = lambda sqrt(log_plus(x)), log_plus(x) = max(ln x, 1): branch-free, exactly
-                // lambda while x <= e (rsqrt(1) = 1); elsewhere within ~1e-7 of the float64 value
-                float b = lam_sc;
-                if (slow) {
-                    const float x = fmaf((float)j, dx, jx0);
-                    const float lp = fmaxf(__log2f(x) * 0.69314718f, 1.f);
-                    b = lam_sc * (lp * rsqrtf(lp));
-                }
                 const float a = fabsf(acc);
                 mx = m ? fmaxf(mx, a) : mx;
-                first = (m && a > b && first == 0) ? t + 1 - n : first;
+                // strict crossing |MO_j| > b_j (_kernels.py:47).  b_j >= lambda: only a date past
+                // lambda before the first crossing needs b_j, and only j >= je needs log_plus (a
+                // call, so the log/rsqrt never run predicated on every date)
+                if (m && first == 0 && a > lam_sc) {
+                    const float b = j >= je ? masked_bound(lam_sc, j, dx, jx0) : lam_sc;
+                    if (a > b) first = t + 1 - n;
+                }
                 msum += m ? acc : 0.f;
                 j += m ? 1 : 0;
                 if (KEEP) {
