@@ -154,6 +154,9 @@ static __device__ const unsigned int kNanRow[1] = {0x7fc00000u};
                             // __syncthreads (measured 5% SLOWER at C2 and C5: the barrier keeps the
                             // four warps' scalar row loads coherent)
 #endif
+#ifndef BWM_MASK_DEFER
+#define BWM_MASK_DEFER 1    // issue a block's Gram MMAs one block later (its TMEM stores have landed)
+#endif
 #ifndef BWM_MASK_MINB
 #define BWM_MASK_MINB 4
 #endif
@@ -218,6 +221,44 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
         for (int64_t q = 0; q < S - 2; ++q) issue_b(q);
     constexpr uint32_t kIdesc = idesc_tf32(NN);
     int64_t q = 0;                                                     // CTA-wide block counter
+    // Gram MMAs of block qq (first date t0q of its tile): every thread's mask row of the block is
+    // in its TMEM lane (A buffer qq % AB) once its tcgen05.st completed; one thread issues
+    // 2 K-steps x 2 splits and commits them to m_done (A buffer free) and b_empty (B stage free).
+    auto issue_mma = [&](int64_t qq, int t0q) {
+        const int abq = (int)(qq % AB);
+        tmem_wait_st();
+        tmem_fence_before();
+        bool issuer;
+        if (BWM_MASK_TICKET) {
+            // the last of the four warps to stage its rows of this block issues the MMAs
+            __syncwarp();
+            uint32_t tk = 0;
+            if ((tid & 31) == 0)
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(tk) : "r"(smem_u32(s_tick + abq)) : "memory");
+            issuer = (__shfl_sync(0xffffffffu, tk, 0) & 3u) == 3u && (tid & 31) == 0;
+        } else {
+            __syncthreads();
+            issuer = tid == 0;
+        }
+        if (issuer) {
+            tmem_fence_after();
+            const int st = (int)(qq % S);
+            mbar_wait(b_full + st, (uint32_t)((qq / S) & 1));
+            const uint32_t bt = sb_u32 + st * SB;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+                for (int sp = 0; sp < 2; ++sp)
+                    mma_tf32_ts(d_col, a_col + 16 * abq + 8 * ks,
+                                smem_desc_kmajor(bt + (2 * ks + sp) * NN * 32, 128, 256), kIdesc,
+                                (t0q > 0 || ks > 0 || sp > 0) ? 1u : 0u);
+            mma_commit(smem_u32(m_done + abq));
+            mma_commit(smem_u32(b_empty + st));
+            // refill the stage of block qq-2 (its MMAs were issued two blocks ago) with block qq+2
+            if (qq >= 2) mbar_wait(b_empty + (int)((qq - 2) % S), (uint32_t)(((qq - 2) / S) & 1));
+            issue_b(qq + S - 2);
+        }
+    };
 
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int64_t px = tile * kMaskTile + tid;
@@ -282,43 +323,20 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
 #pragma unroll
                 for (int i = 0; i < NP / 2; ++i) { two_sum(ghi[i], glo[i], gp[i]); gp[i] = f2(0.f, 0.f); }
             }
-            // A buffer q&1 is free once the MMAs of block q-2 completed
+            // A buffer ab is free once the MMAs of block q - AB completed
             const int ab = (int)(q % AB);
             if (q >= AB) mbar_wait(m_done + ab, (uint32_t)((q / AB - 1) & 1));
-            tmem_st16(a_col + lane_off + 16 * ab, wv);
-            tmem_wait_st();
-            tmem_fence_before();
-            bool issuer;
-            if (BWM_MASK_TICKET) {
-                // the last of the four warps to stage its rows of this block issues the MMAs
-                __syncwarp();
-                uint32_t t = 0;
-                if ((tid & 31) == 0)
-                    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(t) : "r"(smem_u32(s_tick + ab)) : "memory");
-                issuer = (__shfl_sync(0xffffffffu, t, 0) & 3u) == 3u && (tid & 31) == 0;
+            if (BWM_MASK_DEFER) {
+                // block q-1's mask rows were stored at the end of the previous iteration: their
+                // tcgen05.st completed while this block was computed, so the wait is free
+                if (t0 > 0) issue_mma(q - 1, t0 - D);
+                tmem_st16(a_col + lane_off + 16 * ab, wv);
             } else {
-                __syncthreads();
-                issuer = tid == 0;
-            }
-            if (issuer) {
-                tmem_fence_after();
-                const int st = (int)(q % S);
-                mbar_wait(b_full + st, (uint32_t)((q / S) & 1));
-                const uint32_t bt = sb_u32 + st * SB;
-#pragma unroll
-                for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-                    for (int sp = 0; sp < 2; ++sp)
-                        mma_tf32_ts(d_col, a_col + 16 * ab + 8 * ks,
-                                    smem_desc_kmajor(bt + (2 * ks + sp) * NN * 32, 128, 256), kIdesc,
-                                    (t0 > 0 || ks > 0 || sp > 0) ? 1u : 0u);
-                mma_commit(smem_u32(m_done + ab));
-                mma_commit(smem_u32(b_empty + st));
-                // refill the stage of block q-2 (its MMAs were issued two blocks ago) with block q+2
-                if (q >= 2) mbar_wait(b_empty + (int)((q - 2) % S), (uint32_t)(((q - 2) / S) & 1));
-                issue_b(q + S - 2);
+                tmem_st16(a_col + lane_off + 16 * ab, wv);
+                issue_mma(q, t0);
             }
         }
+        if (BWM_MASK_DEFER) issue_mma(q - 1, n16 - D);      // the tile's last block
         // the Gram complement of this tile: wait for the last block's MMAs, read this lane
         mbar_wait(m_done + (int)((q - 1) % AB), (uint32_t)(((q - 1) / AB) & 1));
         tmem_fence_after();
