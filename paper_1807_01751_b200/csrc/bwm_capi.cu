@@ -318,6 +318,7 @@ struct bwm_plan {
     float* d_xx = nullptr;
     double* d_gfull = nullptr;
     float* d_ring = nullptr;           // [sms * bpm_masked][h][128] when mbig
+    double gscale = 0.0;               // exact-digit Gram complement scale (bwm::mask_digits)
     HostPipe pipe;
     std::unique_ptr<bwm::StagedReader> freader;   // bwm_monitor_file: pinned slots + reader pool
     std::mutex mu;                     // serialises bwm_monitor_host on one plan
@@ -420,18 +421,44 @@ static int plan_create_masked(bwm_plan* plan, const bwm_tables* tb, int max_opti
     std::vector<double> gf((size_t)kk, 0.0);
     for (int t = 0; t < N; ++t)
         for (int i = 0; i < p; ++i) xt[(size_t)t * sp + i] = (float)tb->design[(size_t)i * N + t];
+    // x_t x_t^T of the float32 design rows the kernel multiplies with (products of two floats are
+    // exact in float64).  p <= 14 (bwm::mask_digits): two 11-bit fixed-point digits of x x^T / S
+    // (S: a power of two >= max |x x^T|), integer-valued and exact in tf32, accumulated by the
+    // kernel in separate TMEM regions (exact integer sums); Gm = S/2048 (D_hi + D_lo/2048).
+    // p >= 16: tf32 hi + lo of the float32 product in one region.
+    const bool digits = bwm::mask_digits(p);
+    double smax = 0.0;
+    for (int t = 0; t < n; ++t)
+        for (int i = 0; i < p; ++i)
+            for (int j = 0; j <= i; ++j)
+                smax = std::max(smax, std::fabs((double)(float)tb->design[(size_t)i * N + t] *
+                                                (double)(float)tb->design[(size_t)j * N + t]));
+    double gsc = 1.0;
+    while (gsc < smax) gsc *= 2.0;
+    while (smax > 0.0 && gsc / 2.0 >= smax) gsc /= 2.0;
+    plan->gscale = gsc / 2048.0;
     for (int t = 0; t < n; ++t) {
         const int kb = t / bwm::kMaskD, step = (t % bwm::kMaskD) / 8, k = t % 8;
         for (int i = 0; i < p; ++i)
             for (int j = 0; j <= i; ++j) {
                 const int e = i * (i + 1) / 2 + j;
-                const float v = (float)(tb->design[(size_t)i * N + t] * tb->design[(size_t)j * N + t]);
-                const float hi = tf32_round(v), lo = tf32_round(v - hi);
+                const double pr = (double)(float)tb->design[(size_t)i * N + t] * (double)(float)tb->design[(size_t)j * N + t];
+                float hi, lo;
+                if (digits) {
+                    const double u = pr / gsc * 2048.0;             // |u| <= 2048
+                    hi = (float)std::nearbyint(u);
+                    lo = (float)std::nearbyint((u - (double)hi) * 2048.0);
+                    gf[e] += plan->gscale * ((double)hi + (double)lo / 2048.0);
+                } else {
+                    const float v = (float)pr;
+                    hi = tf32_round(v);
+                    lo = tf32_round(v - hi);
+                    gf[e] += (double)hi + (double)lo;
+                }
                 const size_t in_region = (size_t)(e / 8) * 64 + (k / 4) * 32 + (e % 8) * 4 + (k % 4);
                 const size_t base = (size_t)kb * nn * 32 + (size_t)(2 * step) * nn * 8;
                 tiles[base + in_region] = hi;
                 tiles[base + (size_t)nn * 8 + in_region] = lo;
-                gf[e] += (double)hi + (double)lo;
             }
     }
     auto fail = [&](cudaError_t e, const char* what) {
@@ -906,6 +933,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         k.gfull = plan->d_gfull;
         k.ring_g = plan->d_ring;
         k.lambda = plan->lambda;
+        k.gscale = plan->gscale;
         const int64_t tiles = (n_pixels + bwm::kMaskTile - 1) / bwm::kMaskTile;
         const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * plan->bpm_masked);
         pick_masked(d.n_params, plan->mbig, out->mosum != nullptr)<<<(unsigned)grid, bwm::kMaskThreads, (size_t)plan->smem_masked, st>>>(k);

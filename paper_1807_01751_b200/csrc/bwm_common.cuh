@@ -53,6 +53,7 @@ struct KParams {
     const double* gfull;        // [KK] sum of those rows over the whole history
     float* ring_g;              // per-CTA residual rings [grid][h][128] when they live in global memory
     float lambda;               // crit = bound[0]
+    double gscale;              // exact-digit Gram complement: Gm = gscale * (D_hi + D_lo / 2048)
     // long monitoring horizons (LDG kernel): fitted values in float64 from this [N][sp] table
     // (Z^T in double) and the compensated beta_Q, so the trend extrapolation keeps 1e-4
     const double* xtd;          // nullptr: float32 fitted values (the default)

@@ -60,10 +60,19 @@ struct Gram {
 };
 
 __host__ __device__ constexpr int gram_nn(int p) { return ((p * (p + 1) / 2 + 15) / 16) * 16; }
-__host__ __device__ constexpr int masked_tmem_cols(int p) {
-    return gram_nn(p) + 16 * kMaskABufs <= 64 ? 64 : gram_nn(p) + 16 * kMaskABufs <= 128 ? 128
-           : gram_nn(p) + 16 * kMaskABufs <= 256 ? 256 : 512;
+// Exact Gram complement (p <= 14): the x x^T entries are split into two 11-bit fixed-point
+// digits (integer-valued tf32 operands), each digit level accumulated in its own TMEM region:
+// every partial sum is an integer below 2^24, so the float32 accumulation is exact and
+// G_v = G_full - Gm is good to float64 (the round-1 float hi/lo split summed in one float32
+// accumulator carried ~2e-5 of max |MO| at C4/C5).  p >= 16: the float split, one region.
+__host__ __device__ constexpr bool mask_digits(int p) { return p <= 14; }
+__host__ __device__ constexpr int mask_dcols(int p) { return (mask_digits(p) ? 2 : 1) * gram_nn(p); }
+__host__ __device__ constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+// A buffers (16 columns each): 4, or 2 when 4 would double the TMEM allocation
+__host__ __device__ constexpr int mask_ab(int p) {
+    return pow2_cols(mask_dcols(p) + 16 * kMaskABufs) == pow2_cols(mask_dcols(p) + 32) ? kMaskABufs : 2;
 }
+__host__ __device__ constexpr int masked_tmem_cols(int p) { return pow2_cols(mask_dcols(p) + 16 * mask_ab(p)); }
 
 // tcgen05 pieces of the Gram MMA -----------------------------------------------------------
 // Shared-memory matrix descriptor, K-major, no swizzle: core matrices of 8 rows x 16 bytes,
@@ -154,6 +163,10 @@ static __device__ const unsigned int kNanRow[1] = {0x7fc00000u};
                             // __syncthreads (measured 5% SLOWER at C2 and C5: the barrier keeps the
                             // four warps' scalar row loads coherent)
 #endif
+#ifndef BWM_MASK_FAST
+#define BWM_MASK_FAST 1     // shared-memory geometries: refine from the Gram matrix (e = g - G_v beta),
+                            // one-pass RSS; the exact refinement sweep only for flagged pixels
+#endif
 #ifndef BWM_MASK_DEFER
 #define BWM_MASK_DEFER 1    // issue a block's Gram MMAs one block later (its TMEM stores have landed)
 #endif
@@ -165,7 +178,8 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
     monitor_kernel_masked(const __grid_constant__ KParams prm) {
     constexpr int SP = Coefs<NP>::SP;
     constexpr int KK = Gram<NP>::KK, NN = Gram<NP>::NN, SB = Gram<NP>::SB;
-    constexpr int D = kMaskD, S = kMaskBStages, AB = kMaskABufs;
+    constexpr int D = kMaskD, S = kMaskBStages, AB = mask_ab(NP);
+    constexpr bool DIG = mask_digits(NP);
     constexpr int D23 = BWM_MASK_D23;   // dates per register block of passes 2 and 3 (8: C2 -3%, C5 +7%, C4 +60%)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
@@ -199,7 +213,22 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
     tmem_fence_after();
     const uint32_t tbase = *s_tmem;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;            // this warp's TMEM lane quarter
-    const uint32_t d_col = tbase, a_col = tbase + NN;                 // Gm accumulator | AB x 16 A columns
+    // Gm accumulator(s): [hi digits | lo digits] (DIG) or one region | AB x 16 A columns
+    const uint32_t d_col = tbase, a_col = tbase + mask_dcols(NP);
+    // this lane's Gm entries idx in [16 c16, 16 c16 + 16): exact digit sums -> float64
+    auto gm_chunk = [&](int c16, double (&g16)[16]) {
+        float hi[16];
+        tmem_ld16(d_col + lane_off + 16 * c16, *reinterpret_cast<float2(*)[8]>(hi));
+        if (DIG) {
+            float lo[16];
+            tmem_ld16(d_col + NN + lane_off + 16 * c16, *reinterpret_cast<float2(*)[8]>(lo));
+#pragma unroll
+            for (int u = 0; u < 16; ++u) g16[u] = prm.gscale * ((double)hi[u] + (double)lo[u] * (1.0 / 2048.0));
+        } else {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) g16[u] = (double)hi[u];
+        }
+    };
     float* ring = (BIG ? prm.ring_g + (int64_t)blockIdx.x * masked_scratch_words(h, NP, true) * kMaskThreads : s_ring) +
                   tid;
     uint16_t* ring_d = reinterpret_cast<uint16_t*>(ring - tid + h * kMaskThreads) + tid;   // ring dates (!BIG)
@@ -249,9 +278,9 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
             for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
                 for (int sp = 0; sp < 2; ++sp)
-                    mma_tf32_ts(d_col, a_col + 16 * abq + 8 * ks,
+                    mma_tf32_ts(d_col + (DIG ? sp * NN : 0), a_col + 16 * abq + 8 * ks,
                                 smem_desc_kmajor(bt + (2 * ks + sp) * NN * 32, 128, 256), kIdesc,
-                                (t0q > 0 || ks > 0 || sp > 0) ? 1u : 0u);
+                                (t0q > 0 || ks > 0 || (!DIG && sp > 0)) ? 1u : 0u);
             mma_commit(smem_u32(m_done + abq));
             mma_commit(smem_u32(b_empty + st));
             // refill the stage of block qq-2 (its MMAs were issued two blocks ago) with block qq+2
@@ -298,7 +327,9 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
 #pragma unroll
         for (int i = 0; i < NP / 2; ++i) gp[i] = ghi[i] = glo[i] = f2(0.f, 0.f);
         int nv = 0;
+        double qd = 0.0;                         // sum of (y - c)^2 over the valid history dates
         for (int t0 = 0; t0 < n16; t0 += D, ++q) {
+            float qp = 0.f;
             float vb[D];
             load(t0, n, vb);
             float2 wv[D / 2];                                          // 1 = missing: this block's A row
@@ -310,6 +341,7 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
                 have_c = have_c || m;
                 const float yc = m ? vb[k] - c : 0.f;
                 nv += m ? 1 : 0;
+                qp = fmaf(yc, yc, qp);
                 if (k & 1) wv[k >> 1].y = m ? 0.f : 1.f; else wv[k >> 1].x = m ? 0.f : 1.f;
                 const float4* x4 = reinterpret_cast<const float4*>(s_x + t * SP);
 #pragma unroll
@@ -323,6 +355,7 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
 #pragma unroll
                 for (int i = 0; i < NP / 2; ++i) { two_sum(ghi[i], glo[i], gp[i]); gp[i] = f2(0.f, 0.f); }
             }
+            qd += (double)qp;
             // A buffer ab is free once the MMAs of block q - AB completed
             const int ab = (int)(q % AB);
             if (q >= AB) mbar_wait(m_done + ab, (uint32_t)((q / AB - 1) & 1));
@@ -340,11 +373,6 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
         // the Gram complement of this tile: wait for the last block's MMAs, read this lane
         mbar_wait(m_done + (int)((q - 1) % AB), (uint32_t)(((q - 1) / AB) & 1));
         tmem_fence_after();
-        float gmv[NN];
-#pragma unroll
-        for (int c16 = 0; c16 < NN / 16; ++c16)
-            tmem_ld16(d_col + lane_off + 16 * c16, *reinterpret_cast<float2(*)[8]>(&gmv[16 * c16]));
-        tmem_fence_before();      // the next tile's first MMA overwrites D after a __syncthreads
 
         // ---- solve G_v beta' = g: float32 Cholesky in registers (G_v formed in float64) -----
         // Emulated against the float64 oracle: a float32 factor plus the refinement step below
@@ -352,9 +380,14 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
         // cond 30), without the float64 register pressure that spilled through the loops.
         float L[KK], dinv[NP];
 #pragma unroll
-        for (int i = 0; i < KK; ++i) {
-            L[i] = (float)(__ldg(prm.gfull + i) - (double)gmv[i]);
+        for (int c16 = 0; c16 < NN / 16; ++c16) {
+            double g16[16];
+            gm_chunk(c16, g16);
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (16 * c16 + u < KK) L[16 * c16 + u] = (float)(__ldg(prm.gfull + 16 * c16 + u) - g16[u]);
         }
+        tmem_fence_before();      // the next tile's first MMA overwrites D after a __syncthreads
         bool ok = nv > NP;
         chol_col<NP, 0>(L, dinv, ok);
         // L w = b, L^T x = w  (in place)
@@ -396,7 +429,65 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
             return r2.x + r2.y;
         };
 
-        // ---- pass 2: RSS (two-pass) and the refinement residual e = X_v r --------------------
+        // ---- fast refinement (shared-memory geometries): e = g - G_v beta_0 from the Gram matrix --
+        // G_v = G_full - Gm (float64 table minus this lane's TMEM accumulator, still resident: the
+        // next tile's first MMA overwrites it only after a later CTA barrier), one refinement step,
+        // one-pass RSS = q - g^T beta.  A pixel whose RSS cancels (q > 300 RSS) or is not positive
+        // takes the exact path instead (the refinement sweep over its residuals, below); the choice
+        // is per pixel, so results do not depend on the neighbours in the warp.
+        constexpr bool FAST = DIG && !BIG && BWM_MASK_FAST && NP <= 10;   // (register budget)
+        bool needx = true;
+        double rss_f = 0.0;
+        float2 nbf[NP / 2];
+#pragma unroll
+        for (int i = 0; i < NP / 2; ++i) nbf[i] = nb[i];
+        if (FAST) {
+            double gb[NP];                       // G_v beta_0
+#pragma unroll
+            for (int i = 0; i < NP; ++i) gb[i] = 0.0;
+#pragma unroll
+            for (int c16 = 0; c16 < NN / 16; ++c16) {
+                double gm16[16];
+                gm_chunk(c16, gm16);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int idx = 16 * c16 + u;
+                    if (idx < KK) {
+                        // packed lower triangle: idx = i(i+1)/2 + j, j <= i
+                        int i = 0;
+#pragma unroll
+                        for (int ii = 1; ii < NP; ++ii) i += (idx >= ii * (ii + 1) / 2) ? 1 : 0;
+                        const int j = idx - i * (i + 1) / 2;
+                        const double gv = __ldg(prm.gfull + idx) - gm16[u];
+                        const double bj = -(double)((j & 1) ? nb[j >> 1].y : nb[j >> 1].x);
+                        const double bi = -(double)((i & 1) ? nb[i >> 1].y : nb[i >> 1].x);
+                        gb[i] += gv * bj;
+                        if (i != j) gb[j] += gv * bi;
+                    }
+                }
+            }
+            float d[NP];
+            double gd[NP];
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                const float2 gg = ghi[i >> 1], gl = glo[i >> 1];
+                gd[i] = (i & 1) ? (double)gg.y + (double)gl.y : (double)gg.x + (double)gl.x;
+                d[i] = (float)(gd[i] - gb[i]);
+            }
+            tmem_fence_before();                 // the re-read precedes the next tile's first MMA
+            chol_solve(d);
+            double gbeta = 0.0;
+#pragma unroll
+            for (int i = 0; i < NP / 2; ++i) {
+                nbf[i] = sub2(nb[i], f2(d[2 * i], d[2 * i + 1]));
+                gbeta += gd[2 * i] * -(double)nbf[i].x + gd[2 * i + 1] * -(double)nbf[i].y;
+            }
+            rss_f = qd - gbeta;
+            needx = ok && !(rss_f > 0.0 && qd <= 300.0 * rss_f);
+        }
+        const bool anyx = !FAST || __any_sync(0xffffffffu, needx);
+
+        // ---- pass 2 (exact path): RSS (two-pass) and the refinement residual e = X_v r ---------
         const int hv = (int)(((int64_t)h * nv) / n);
         const int wfirst = nv - hv + 1;          // 0-based compacted index of window 0's first element
         constexpr int RS = kMaskThreads;         // ring row stride (words)
@@ -407,7 +498,7 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
         float2 e2[NP / 2];                       // X_v r (normal-equation residual)
 #pragma unroll
         for (int i = 0; i < NP / 2; ++i) e2[i] = f2(0.f, 0.f);
-        for (int t0 = 0; t0 < n; t0 += D23) {
+        for (int t0 = 0; anyx && t0 < n; t0 += D23) {
             float vb[D23];
             load(t0, n, vb);
             float part = 0.f;
@@ -428,7 +519,7 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
                 if (BIG) {
                     tw = (m && seen == wfirst) ? t : tw;
                 } else {                         // shared-memory ring: window 0 written here
-                    const bool inwin = m && seen >= wfirst;
+                    const bool inwin = m && seen >= wfirst && needx;
                     if (inwin) {
                         ring[so] = r;
                         ring_d[so] = (uint16_t)t;
@@ -468,10 +559,14 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
         float2 nb0[NP / 2];                      // pre-refinement -beta' (window-0 residuals, BIG)
 #pragma unroll
         for (int i = 0; i < NP / 2; ++i) nb0[i] = nb[i];
-        if (ok) {
+        if (ok && needx) {
             rss = fmax(rss - 2.0 * de + quad, 0.0);
 #pragma unroll
             for (int i = 0; i < NP / 2; ++i) nb[i] = sub2(nb[i], f2(db[2 * i], db[2 * i + 1]));
+        } else if (ok) {                         // fast path
+            rss = rss_f;
+#pragma unroll
+            for (int i = 0; i < NP / 2; ++i) nb[i] = nbf[i];
         }
 
         // ---- window 0: the last hv - 1 valid history residuals, corrected by the refinement ---
@@ -491,6 +586,28 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
                 for (int i = 0; i < NP; ++i) r = fmaf(-db[i], xr[i], r);
                 ring[s2 * kMaskThreads] = r;
                 acc += r;
+            }
+            // fast-path pixels: the last hv - 1 valid history residuals with the refined beta, by a
+            // backward sweep from n - 1 that stops once every such lane of the warp has its window
+            int rem = (FAST && ok && !needx && hv >= 2) ? hv - 1 : 0;
+            if (FAST && __any_sync(0xffffffffu, rem > 0)) {
+                int sidx = (hv - 1) * RS;
+                float accw = 0.f;
+                for (int t0 = ((n - 1) / D23) * D23; t0 >= 0 && __any_sync(0xffffffffu, rem > 0); t0 -= D23) {
+                    float vb[D23];
+                    load(t0, n, vb);
+#pragma unroll
+                    for (int k = D23 - 1; k >= 0; --k) {
+                        const int t = t0 + k;
+                        const bool inwin = rem > 0 && finitef(vb[k]) && t < n;
+                        const float r = resid(inwin ? vb[k] - c : 0.f, t);
+                        if (inwin) ring[sidx] = r;
+                        sidx -= inwin ? RS : 0;
+                        rem -= inwin ? 1 : 0;
+                        accw += inwin ? r : 0.f;
+                    }
+                }
+                if (ok && !needx) acc = accw;
             }
         } else {
             int tlo = tw;
