@@ -936,7 +936,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         k.gscale = plan->gscale;
         const int64_t tiles = (n_pixels + bwm::kMaskTile - 1) / bwm::kMaskTile;
         const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * plan->bpm_masked);
-        pick_masked(d.n_params, plan->mbig, out->mosum != nullptr)<<<(unsigned)grid, bwm::kMaskThreads, (size_t)plan->smem_masked, st>>>(k);
+        pick_masked(d.n_params, plan->mbig, out->mosum != nullptr || out->mo_mean != nullptr)<<<(unsigned)grid, bwm::kMaskThreads, (size_t)plan->smem_masked, st>>>(k);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_err((int)e, "kernel launch failed: %s", cudaGetErrorString(e));
         ++launched;

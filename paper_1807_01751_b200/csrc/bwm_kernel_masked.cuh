@@ -691,7 +691,8 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
         int ro = 0;                              // word offset of the ring slot holding r_{e - h_v}
         const int ro_end = hv * RS;
         const float jx0 = (float)(nv + 1) * inv_nv, dx = inv_nv;   // x_j = (n_v + 1 + j) / n_v
-        float* mo_p = KEEP ? prm.mosum + px : nullptr;
+        // KEEP: the MOSUM matrix and/or the MOSUM mean were requested (the LEAN variant skips both)
+        float* mo_p = KEEP && prm.mosum ? prm.mosum + px : nullptr;
         const int64_t ld_out = prm.ld_out;
         // log_plus(x) = 1 while x = (n_v + 1 + j) / n_v <= e, i.e. j < je: b_j = lambda exactly
         const int je = fit_ok ? (int)floorf(1.718281828f * (float)nv - 1.f) + 1 : 0x3fffffff;
@@ -717,9 +718,9 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
                     const float b = j >= je ? masked_bound(lam_sc, j, dx, jx0) : lam_sc;
                     if (a > b) first = t + 1 - n;
                 }
-                msum += m ? acc : 0.f;
+                if (KEEP) msum += m ? acc : 0.f;
                 j += m ? 1 : 0;
-                if (KEEP) {
+                if (KEEP && mo_p) {
                     if (act && t < N) *mo_p = m ? acc * inv : qnan;
                     mo_p += ld_out;
                 }
