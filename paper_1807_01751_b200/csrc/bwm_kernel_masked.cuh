@@ -497,7 +497,8 @@ __global__ void __launch_bounds__(kMaskThreads, NP <= 8 ? BWM_MASK_MINB : 2)
             // The Gram-matrix refinement leaves beta with the float32 error of g (~3e-7 relative), a
             // few 1e-6 of MO absolute: invisible at rtol 1e-4 unless max |MO| is tiny, which takes a
             // monitoring period of a handful of dates.  Short periods (N - n < 64) stay exact.
-            const bool geom = N - n >= 64;
+            // (and the digit sums stay exact integers below 2^24: n < 8192 history dates)
+            const bool geom = N - n >= 64 && n16 <= 8192;
             needx = ok && (BWM_MASK_FORCEX || !geom || !(rss_f > 0.0 && qd <= 300.0 * rss_f && wellcond));
         }
         const bool anyx = !FAST || __any_sync(0xffffffffu, needx);
