@@ -84,6 +84,9 @@ constexpr bool kMirror = BWM_RING_MIRROR != 0;
 // the lagging-cursor mode moves two boxes per stage (dates t and t-h): 3 stages = 6 boxes
 // (kRingLag: tables in global memory, 3 stages, 3 CTAs/SM; kRingLagT: tables in smem, 2 stages,
 //  2 CTAs/SM — measured 8.85 vs 8.11 ms at C4, so kRingLagT whenever its tables fit)
+#ifndef BWM_LAG_TMEMC
+#define BWM_LAG_TMEMC 1    // kRingLagT: park pass 1's compensated beta_Q (hi, lo) in Tensor Memory (C4: 5.45 -> 5.23 ms, no spills)
+#endif
 #ifndef BWM_STAGES_LAGT
 #define BWM_STAGES_LAGT 2
 #endif
@@ -225,6 +228,26 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float2 (&v)[8]) 
         "r"(__float_as_uint(v[7].y))
         : "memory");
 }
+// the first NP float2 of a 32-column run of this thread's lane: .x16 pieces plus a tail
+template <int NP>
+__device__ __forceinline__ void tmem_ld_pairs(uint32_t taddr, float2 (&v)[NP]) {
+    float2 a[8], b[8];                   // (callers use NP <= 16)
+    tmem_ld16(taddr, a);                 // includes wait::ld
+    if (NP > 8) tmem_ld16(taddr + 16, b);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) v[i] = i < 8 ? a[i] : i < 16 ? b[i - 8] : f2(0.f, 0.f);
+}
+template <int NP>
+__device__ __forceinline__ void tmem_st_pairs(uint32_t taddr, const float2 (&v)[NP]) {
+    float2 a[8], b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        a[i] = i < NP ? v[i] : f2(0.f, 0.f);
+        b[i] = i + 8 < NP ? v[i + 8] : f2(0.f, 0.f);
+    }
+    tmem_st16(taddr, a);
+    if (NP > 8) tmem_st16(taddr + 16, b);
+}
 __device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(__float_as_uint(v.x)),
                  "r"(__float_as_uint(v.y))
@@ -311,10 +334,16 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
             for (int s = 0; s < S; ++s) s_tick[s] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (MODE == kRingTmem && threadIdx.x < 32) tmem_alloc(s_tmem, (uint32_t)prm.tmem_cols);
-    if (MODE == kRingTmem) tmem_fence_before();
+    // kPark: pass 1's compensated beta_Q (hi, lo) lives in Tensor Memory (the lagging cursor has
+    // no ring there), freeing 4 NP registers: 64 columns per warp (hi | lo, 32 each) in its lane
+    // quarter; the 16+-warp CTA owns the SM, so it takes all 512 columns
+    constexpr bool kPark = MODE == kRingLagT && BWM_LAG_TMEMC && NP <= 16 && BWM_LAGT_WARPS > 4;
+    constexpr bool kTmem = MODE == kRingTmem || kPark;
+    const uint32_t tmem_cols = MODE == kRingTmem ? (uint32_t)prm.tmem_cols : 512u;
+    if (kTmem && threadIdx.x < 32) tmem_alloc(s_tmem, tmem_cols);
+    if (kTmem) tmem_fence_before();
     __syncthreads();
-    if (MODE == kRingTmem) tmem_fence_after();
+    if (kTmem) tmem_fence_after();
 
     const int64_t n_tiles = prm.n_pixels / TILE;       // host guarantees whole tiles
     const int64_t ld = prm.ld_y;
@@ -367,6 +396,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
 
     const int L = prm.ring_rows;
     const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(wu * 32) << 16) : 0u;
+    const uint32_t pbase = kPark ? *s_tmem + ((uint32_t)((wu & 3) * 32) << 16) + (uint32_t)((wu >> 2) * 64) : 0u;
     auto tcol = [&](int row) -> uint32_t { return tbase + (uint32_t)(2 * row); };
     // ring row q of time t is t mod L (2 columns per row: 2L columns, no mirror rows)
     // ring rows of the fixed dates of every tile (one modulo each, per CTA)
@@ -444,6 +474,10 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         float2 hi[NP], lo[NP], part[NP];
 #pragma unroll
         for (int i = 0; i < NP; ++i) { hi[i] = lo[i] = part[i] = f2(0.f, 0.f); }
+        if (kPark) {
+            tmem_st_pairs<NP>(pbase, hi);
+            tmem_st_pairs<NP>(pbase + 32, lo);
+        }
         float2 qpart = f2(0.f, 0.f), wpart = f2(0.f, 0.f);
         double q0 = 0.0, q1 = 0.0, wd0 = 0.0, wd1 = 0.0;   // ||y-c||^2, window sum of [n-h, n)
         float2 c = f2(0.f, 0.f);
@@ -510,8 +544,19 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
             release();
             if (park) { pr += R; if (pr >= L) pr -= L; }
             if (((t0 + R) & (kComp - 1)) == 0 || t0 + R >= n) {
+                if (kPark) {
+                    float2 h2[NP], l2[NP];
+                    tmem_wait_st();
+                    tmem_ld_pairs<NP>(pbase, h2);
+                    tmem_ld_pairs<NP>(pbase + 32, l2);
 #pragma unroll
-                for (int i = 0; i < NP; ++i) { two_sum(hi[i], lo[i], part[i]); part[i] = f2(0.f, 0.f); }
+                    for (int i = 0; i < NP; ++i) { two_sum(h2[i], l2[i], part[i]); part[i] = f2(0.f, 0.f); }
+                    tmem_st_pairs<NP>(pbase, h2);
+                    tmem_st_pairs<NP>(pbase + 32, l2);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) { two_sum(hi[i], lo[i], part[i]); part[i] = f2(0.f, 0.f); }
+                }
                 q0 += (double)qpart.x;
                 q1 += (double)qpart.y;
                 wd0 += (double)wpart.x;
@@ -520,6 +565,11 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
             }
         }
         const bool valid0 = f0, valid1 = f1;
+        if (kPark) {
+            tmem_wait_st();
+            tmem_ld_pairs<NP>(pbase, hi);
+            tmem_ld_pairs<NP>(pbase + 32, lo);
+        }
         float2 bq[NP], nb[NP];    // beta_Q and -beta_Q
 #pragma unroll
         for (int i = 0; i < NP; ++i) { bq[i] = add2(hi[i], lo[i]); nb[i] = f2(-bq[i].x, -bq[i].y); }
@@ -658,12 +708,12 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         if (prm.beta) store_beta<NP>(prm, px0, c, bq, valid0, valid1, 2);
     }
 
-    if (MODE == kRingTmem) {
+    if (kTmem) {
         tmem_wait_st();
         tmem_fence_before();
         __syncthreads();
         tmem_fence_after();
-        if (warp == 0) tmem_dealloc(*s_tmem, (uint32_t)prm.tmem_cols);
+        if (warp == 0) tmem_dealloc(*s_tmem, tmem_cols);
     }
 }
 
