@@ -35,7 +35,10 @@ def main():
         return float(r[i].replace(",", "")) * SCALE.get(units[i], 1)
 
     def pct(k):
-        return float(r[hdr.index(k)].replace(",", "")) if k in hdr else None
+        try:
+            return float(r[hdr.index(k)].replace(",", "")) if k in hdr else None
+        except ValueError:                     # "no data" (a pipe the kernel never used)
+            return None
 
     dram = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
     entry = {
