@@ -51,6 +51,8 @@ def main():
             units[hdr.index("gpu__time_duration.sum")], 1.0),
         "tensor_pipe": {
             "tensor_cycles_active_pct": pct("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+            "tensor_inst_pct": pct("sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active"),
+            "tensor_mem_cycles_active_pct": pct("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
             "fma_cycles_active_pct": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
             "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "source": "ncu --set full, same capture",
