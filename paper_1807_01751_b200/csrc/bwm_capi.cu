@@ -698,12 +698,15 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
     std::vector<double> wtd((size_t)N * sp, 0.0);
     for (int t = 0; t < n; ++t)
         for (int i = 0; i < p; ++i) wtd[(size_t)t * sp + i] = Q[(size_t)t * p + i];
-    for (int t = n; t < N; ++t)
-        for (int i = 1; i < p; ++i) {
-            double s = 0.0;
-            for (int u = t - h + 1; u <= t; ++u) s += xtd[(size_t)u * sp + i];
+    for (int i = 1; i < p; ++i) {          // sliding window sum, O(N p) (long series)
+        double s = 0.0;
+        for (int u = n - h + 1; u <= n; ++u) s += xtd[(size_t)u * sp + i];
+        wtd[(size_t)n * sp + i] = s;
+        for (int t = n + 1; t < N; ++t) {
+            s += xtd[(size_t)t * sp + i] - xtd[(size_t)(t - h) * sp + i];
             wtd[(size_t)t * sp + i] = s;
         }
+    }
     plan->s0 = (double)h * Rinv[0];
     std::vector<float> wt(wtd.size());
     for (size_t i = 0; i < wt.size(); ++i) wt[i] = (float)wtd[i];

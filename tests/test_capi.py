@@ -96,3 +96,31 @@ def test_sass_contains_blackwell_async_copy_and_tensor_memory():
                                        text=True).stdout
     for mnemonic in ("UTMALDG", "LDTM", "STTM", "FFMA2", "SYNCS"):
         assert mnemonic in out, mnemonic
+
+
+@pytest.mark.gpu
+def test_plan_requires_intercept_design_row():
+    """bwm_tables documents design row 0 as the intercept (1 at every date): the window-sum
+    formulation folds that row's window sum into a constant, so a plan with another row 0 is
+    refused (BWM_E_DIMS) rather than computed wrongly."""
+    import numpy as np
+
+    from paper_1807_01751_b200 import _lib
+
+    lib = _lib.load()
+    N, n, h, p = 60, 30, 10, 4
+    t = np.arange(1.0, N + 1)
+    design = np.ascontiguousarray(np.stack([np.ones(N), (t - 15.5) / 14.5, np.sin(t / 3), np.cos(t / 3)]))
+    bound = np.full(N - n, 3.0)
+    dbl = C.POINTER(C.c_double)
+    dims = _lib.Dims(N, n, h, p, 0)
+    plan = C.c_void_p()
+    ok = _lib.Tables(design.ctypes.data_as(dbl), bound.ctypes.data_as(dbl), 15.5, 14.5)
+    assert lib.bwm_plan_create(C.byref(dims), C.byref(ok), 0, C.byref(plan)) == 0
+    lib.bwm_plan_destroy(plan)
+    bad = design.copy()
+    bad[0, 7] = 2.0
+    tb = _lib.Tables(bad.ctypes.data_as(dbl), bound.ctypes.data_as(dbl), 15.5, 14.5)
+    plan = C.c_void_p()
+    assert lib.bwm_plan_create(C.byref(dims), C.byref(tb), 0, C.byref(plan)) == -2
+    assert b"intercept" in lib.bwm_last_error()
