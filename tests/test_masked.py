@@ -233,3 +233,32 @@ def test_gpu_masked_zero_sigma_raises():
     t = np.arange(1.0, y.shape[0] + 1)
     with pytest.raises(pkg.ZeroResidualError, match=r"pixel 5 fits its history exactly"):
         pkg.monitor_batch(pkg.SeriesStack(y, pkg.TimeAxis(t)), _config((100, 50, 3, 23.0, 4.9)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunk", ["1024", "2560"])
+def test_gpu_masked_global_scratch_chunked_pipeline(monkeypatch, chunk):
+    """Masked mode on a global-scratch geometry (p = 14, h = 250: the x x^T table and the
+    residual rings live in plan-owned global memory) through the chunked host pipeline, two
+    chunks in flight on two streams.  Every launch that uses the plan's scratch (rings, float64
+    fixup list) is ordered after the previous one, so the chunked run equals the one-launch run
+    bit for bit, and matches the oracle."""
+    from paper_1807_01751_b200.device import DevicePlan
+
+    pkg = _pkg()
+    N, n, h, k, freq = 1000, 500, 250, 6, 365.25
+    t = np.cumsum(np.random.default_rng(1).uniform(1.0, 9.0, N)) + 1.0
+    y = _gap_stack(3000, t, freq, n, 0.5, 77)
+    args = (n, h, k, freq, 3.0)
+    assert DevicePlan.get(pkg.TimeAxis(t), freq, k, n, h, 3.0, nan_mode="mask").info()["masked_global"] == 1
+    stack = pkg.SeriesStack(y, pkg.TimeAxis(t))
+    whole = pkg.monitor_batch(stack, _config(args), return_beta=True, return_mean=True)
+    monkeypatch.setenv("BWM_HOST_CHUNK", chunk)
+    parts = pkg.monitor_batch(stack, _config(args), return_beta=True, return_mean=True)
+    monkeypatch.delenv("BWM_HOST_CHUNK")
+    for f in ("valid", "first_break", "max_abs_mo", "mosum_mean", "beta"):
+        assert np.array_equal(getattr(whole, f), getattr(parts, f), equal_nan=True), f
+    sl = slice(0, 400)
+    r = oracle_masked(y[:, sl], t, *args)
+    compare("global scratch, chunked", r.first_break, r.max_abs_mo, r.valid, parts.first_break[sl],
+            parts.max_abs_mo[sl], parts.valid[sl], r.near)
