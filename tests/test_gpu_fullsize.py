@@ -86,3 +86,54 @@ def test_fullsize_shift_and_shards(name):
     hi = _maps(plan.run_device(y[:, cut:], pixel_offset=cut))
     for a, b, c in zip(base, lo, hi):
         assert np.array_equal(a, np.concatenate([b, c]))
+
+
+def _masked_plan(w, t):
+    from paper_1807_01751_b200.device import DevicePlan
+    from paper_1807_01751_b200.model import TimeAxis
+
+    return DevicePlan(TimeAxis(t), w.freq, w.harmonics, w.n_hist, w.bandwidth, w.crit, "cuda", nan_mode="mask")
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_fullsize_masked_sample_against_oracle(name):
+    """nan_mode="mask" on the whole stack — C2: shared-memory residual rings,
+    C4: the global-scratch variant (p = 14, h = 250) — and a 3,000-pixel sample against the
+    per-pixel masked oracle: valid identical, first break identical off the boundary, max |MO|
+    within rtol 1e-4."""
+    import torch
+
+    w, t, _, y = _setup(name)
+    plan = _masked_plan(w, t)
+    assert plan.info()["masked_global"] == (1 if name == "C4" else 0)
+    valid, first, mx = _maps(plan.run_device(y))
+    rng = np.random.default_rng(11)
+    idx = np.sort(rng.choice(w.n_pixels, size=3000, replace=False))
+    ys = y[:, torch.as_tensor(idx, device="cuda")].cpu().numpy()
+    del y
+    torch.cuda.empty_cache()
+    ref = bo.monitor_masked(ys, t, w.n_hist, w.bandwidth, w.harmonics, w.freq, w.crit)
+    assert np.array_equal(valid[idx].astype(bool), ref.valid)
+    bad = np.flatnonzero((first[idx] != ref.first_idx) & ~ref.near & ref.valid)
+    assert bad.size == 0, f"{bad.size} non-borderline mismatches, e.g. pixels {idx[bad[:5]]}"
+    np.testing.assert_allclose(mx[idx][ref.valid], ref.max_abs_mo[ref.valid], rtol=RTOL, atol=0)
+    assert valid.mean() > 0.99
+
+
+def test_fullsize_masked_shift_and_shards():
+    """The placement invariance of test_fullsize_shift_and_shards for the masked kernel at C2:
+    one pixel per thread, but warp-wide decisions (the backward window sweep, the exact-sweep
+    lanes) and the per-tile Gram MMAs must not leak between pixels."""
+    w, t, _, y = _setup("C2")
+    plan = _masked_plan(w, t)
+    P = w.n_pixels
+    base = _maps(plan.run_device(y))
+    s = 128 * 1001 + 37
+    got = _maps(plan.run_device(y[:, s:], pixel_offset=s))
+    for a, b in zip(base, got):
+        assert np.array_equal(a[s:], b)
+    cut = P // 3 + 5
+    lo = _maps(plan.run_device(y[:, :cut]))
+    hi = _maps(plan.run_device(y[:, cut:], pixel_offset=cut))
+    for a, b, c in zip(base, lo, hi):
+        assert np.array_equal(a, np.concatenate([b, c]))
