@@ -805,7 +805,8 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
             // TMEM (reports 1).  Allocation is dynamic (tcgen05.alloc + relinquish_alloc_permit),
             // so residency is bounded by registers, shared memory, threads and our own column
             // budget: 512 columns per SM / tmem_cols per CTA.
-            nb = resident_ctas((const void*)fn, threads_of(kind, plan->tring.mode), sm, plan->tring.cols, device, &err);
+            nb = resident_ctas((const void*)fn, threads_of(kind, plan->tring.mode), sm,
+                               plan->tring.cols * (bwm::tma_warps(bwm::kRingTmem) / 4), device, &err);
             if (err != cudaSuccess) return err;
         }
         *nb_out = nb;

@@ -51,6 +51,9 @@ namespace bwm {
 #ifndef BWM_STAGE_ROWS
 #define BWM_STAGE_ROWS 8
 #endif
+#ifndef BWM_TMA_ABL
+#define BWM_TMA_ABL 0      // timing ablation: the stage pipeline without the arithmetic (results wrong)
+#endif
 #ifndef BWM_STAGES
 #define BWM_STAGES 5
 #endif
@@ -260,13 +263,20 @@ __device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
 #ifndef BWM_TMA_MINB_BIG
 #define BWM_TMA_MINB_BIG 3
 #endif
-// Warps per CTA: 4, or BWM_LAGT_WARPS for the lagging cursor with staged tables (C4: the 64 KB
-// Z^T table is shared by more warps, so more warps fit per SM); the tile is 64 px per warp.
-__host__ __device__ constexpr int tma_warps(int mode) { return mode == kRingLagT ? BWM_LAGT_WARPS : kWarps; }
+#ifndef BWM_RING_WARPS
+#define BWM_RING_WARPS 4   // warps per CTA of the TMEM-ring kernel (multiple of 4: a warp per lane quarter
+#endif                     // and TMEM column block)
+// Warps per CTA: BWM_RING_WARPS (TMEM ring), 4 (lagging cursor through L1), or BWM_LAGT_WARPS
+// for the lagging cursor with staged tables (C4: the 64 KB Z^T table is shared by more warps,
+// so more warps fit per SM); the tile is 64 px per warp.
+__host__ __device__ constexpr int tma_warps(int mode) {
+    return mode == kRingLagT ? BWM_LAGT_WARPS : mode == kRingTmem ? BWM_RING_WARPS : kWarps;
+}
 __host__ __device__ constexpr int tma_threads(int mode) { return 32 * tma_warps(mode); }
 __host__ __device__ constexpr int tma_tile(int mode) { return kWarpPx * tma_warps(mode); }
 __host__ __device__ constexpr int tma_minb(int np, int mode) {
-    return mode == kRingLagT ? (BWM_LAGT_WARPS > 4 ? 1 : 2) : np <= 10 ? BWM_TMA_MINB : BWM_TMA_MINB_BIG;
+    return mode == kRingLagT ? (BWM_LAGT_WARPS > 4 ? 1 : 2)
+                             : (np <= 10 ? BWM_TMA_MINB : BWM_TMA_MINB_BIG) * 4 / tma_warps(mode);
 }
 
 // Shared-memory footprint per warp stage (host mirror in bwm_capi.cu); with BWM_SHARED_BOX the
@@ -298,7 +308,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     constexpr bool SHB = BWM_SHARED_BOX != 0;
     constexpr int ROWF2 = (SHB ? TILE : kWarpPx) / 2;    // float2 per staged row
     constexpr int64_t SBX = SHB ? SB * NW : SB;          // bytes of one stage slot
-    static_assert(MODE != kRingTmem || NW == 4, "TMEM ring: one TMEM lane quarter per warp");
+    static_assert(MODE != kRingTmem || NW % 4 == 0, "TMEM ring: warps in whole lane quarters");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
     const int NA = (N + 3) & ~3;
@@ -339,7 +349,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     // quarter; the 16+-warp CTA owns the SM, so it takes all 512 columns
     constexpr bool kPark = MODE == kRingLagT && BWM_LAG_TMEMC && NP <= 16 && BWM_LAGT_WARPS > 4;
     constexpr bool kTmem = MODE == kRingTmem || kPark;
-    const uint32_t tmem_cols = MODE == kRingTmem ? (uint32_t)prm.tmem_cols : 512u;
+    const uint32_t tmem_cols = MODE == kRingTmem ? (uint32_t)prm.tmem_cols * (NW / 4) : 512u;
     if (kTmem && threadIdx.x < 32) tmem_alloc(s_tmem, tmem_cols);
     if (kTmem) tmem_fence_before();
     __syncthreads();
@@ -395,7 +405,9 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     for (int s = 0; s < S; ++s) issue_into(s, !SHB || wu == 0);
 
     const int L = prm.ring_rows;
-    const uint32_t tbase = MODE == kRingTmem ? *s_tmem + ((uint32_t)(wu * 32) << 16) : 0u;
+    const uint32_t tbase = MODE == kRingTmem
+                               ? *s_tmem + ((uint32_t)((wu & 3) * 32) << 16) + (uint32_t)((wu >> 2) * prm.tmem_cols)
+                               : 0u;
     const uint32_t pbase = kPark ? *s_tmem + ((uint32_t)((wu & 3) * 32) << 16) + (uint32_t)((wu >> 2) * 64) : 0u;
     auto tcol = [&](int row) -> uint32_t { return tbase + (uint32_t)(2 * row); };
     // ring row q of time t is t mod L (2 columns per row: 2L columns, no mirror rows)
@@ -488,6 +500,16 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         int pr = q_w0;                                    // ring row of the next parked stage
         for (int t0 = 0; t0 < n; t0 += R) {
             const float2* st = acquire();
+#if BWM_TMA_ABL
+            {   // timing ablation (results wrong): consume the stage, no arithmetic
+                float2 sacc = f2(0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < R; ++k) sacc = add2(sacc, st[k * ROWF2]);
+                last = add2(last, sacc);
+                release();
+                continue;
+            }
+#endif
             if (t0 == 0) {
                 // pass 0: first finite value (engine.py:316 first = finite.argmax)
                 const int rows = min(R, n);
@@ -620,6 +642,16 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         int rb = q_t3h;                                  // ring row of t0 - h
         for (int t0 = t3; t0 < N; t0 += R) {
             const float2* st = acquire();
+#if BWM_TMA_ABL
+            {   // timing ablation (results wrong): consume the stage, no arithmetic
+                float2 sacc = f2(0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < R; ++k) sacc = add2(sacc, st[k * ROWF2]);
+                mx = add2(mx, sacc);
+                release();
+                continue;
+            }
+#endif
             const float2* lst = st + kBox / 8;           // lag dates (kRingLag): second box
             if (t0 >= n && t0 + R <= N) {
                 float2 oldv[R], newv[R];
