@@ -141,7 +141,7 @@ int64_t smem_bytes_tma(int N, int n, int h, int p, int mode) {
     const int S = bwm::stages_for(mode);
     int64_t bytes = bwm::tma_stage_region(mode, S) + fl * 4;
     const int sched = 2 * ((N + bwm::kStageRows - 1) / bwm::kStageRows) + 4;   // stage schedule table
-    return bytes + bwm::tma_barriers(mode, S) * 8 + (BWM_SHARED_BOX ? 4 * S : 0) + 16 + 4 * sched;  // + stage barriers, tickets, TMEM slot
+    return bytes + bwm::tma_barriers(mode, S) * 8 + 16 + 4 * sched;  // + stage barriers, TMEM slot, schedule
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed).
@@ -1024,7 +1024,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * bpm);
         const size_t sm = (size_t)(kind == kTma ? plan->smem_tma : plan->smem);
         if (kind == kTma) {
-            int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y, BWM_SHARED_BOX ? (int)tile : bwm::kWarpPx);
+            int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y, bwm::kWarpPx);
             if (rc) return rc;
         }
         fn<<<(unsigned)grid, threads_of(kind, plan->tring.mode), sm, st>>>(kp);

@@ -77,9 +77,6 @@ constexpr int kStages = BWM_STAGES;             // stage ring depth per warp (TM
 #define BWM_LAZY_CROSS 1   // LEAN: first-crossing search once per stage from the running max
 #endif
 constexpr bool kMirror = BWM_RING_MIRROR != 0;
-#ifndef BWM_SHARED_BOX
-#define BWM_SHARED_BOX 0   // 1: one CTA-wide 256-px box per stage (1 KB rows), re-armed by the last warp to release it
-#endif
 #ifndef BWM_LAGT_WARPS
 #define BWM_LAGT_WARPS 16  // warps per CTA of the lagging-cursor kernel with smem tables (tables shared by all;
                            // C4: 16 warps x 2 stages at 1 CTA/SM 5.27 ms, 8 warps 5.87 (3 stages), 4 warps x 2 CTAs 6.09)
@@ -279,16 +276,15 @@ __host__ __device__ constexpr int tma_minb(int np, int mode) {
                              : (np <= 10 ? BWM_TMA_MINB : BWM_TMA_MINB_BIG) * 4 / tma_warps(mode);
 }
 
-// Shared-memory footprint per warp stage (host mirror in bwm_capi.cu); with BWM_SHARED_BOX the
-// stages are CTA-wide (tma_stage_slots warps' worth each, one slot set per CTA).
+// Shared-memory footprint per warp stage (host mirror in bwm_capi.cu).
 __host__ __device__ constexpr int64_t tma_stage_bytes(int mode) {
     return (int64_t)kBoxBytes * (mode == kRingLag || mode == kRingLagT ? 2 : 1);
 }
 __host__ __device__ constexpr int64_t tma_stage_region(int mode, int stages) {
-    return (int64_t)tma_warps(mode) * stages * tma_stage_bytes(mode);   // same bytes either way
+    return (int64_t)tma_warps(mode) * stages * tma_stage_bytes(mode);
 }
 __host__ __device__ constexpr int tma_barriers(int mode, int stages) {
-    return BWM_SHARED_BOX ? stages : tma_warps(mode) * stages;
+    return tma_warps(mode) * stages;
 }
 
 // LEAN: no MOSUM matrix / MOSUM mean outputs and a constant boundary over the monitoring
@@ -305,9 +301,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     constexpr int S = stages_for(MODE);
     constexpr int64_t SB = tma_stage_bytes(MODE);
     constexpr int NW = tma_warps(MODE), NT = tma_threads(MODE), TILE = tma_tile(MODE);
-    constexpr bool SHB = BWM_SHARED_BOX != 0;
-    constexpr int ROWF2 = (SHB ? TILE : kWarpPx) / 2;    // float2 per staged row
-    constexpr int64_t SBX = SHB ? SB * NW : SB;          // bytes of one stage slot
+    constexpr int ROWF2 = kWarpPx / 2;                   // float2 per staged row
     static_assert(MODE != kRingTmem || NW % 4 == 0, "TMEM ring: warps in whole lane quarters");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int N = prm.N, n = prm.n, h = prm.h;
@@ -322,9 +316,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     const float* s_xt = kTblSmem ? s_tbl : prm.wt;
     const float* s_mt = s_xt;
     float* s_bd = s_tbl + (kTblSmem ? N * SP : 0);                       // [NA] bound by row t (t >= n)
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);           // [NW][S] (SHB: [S])
-    uint32_t* s_tick = reinterpret_cast<uint32_t*>(s_bar + tma_barriers(MODE, S));   // SHB: [S] release tickets
-    uint32_t* s_tmem = s_tick + (SHB ? S : 0);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_bd + NA);           // [NW][S]
+    uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + tma_barriers(MODE, S));
     int* s_rows = reinterpret_cast<int*>(s_tmem + 4);                   // [tile_stages] stage -> first date
 
     if (kTblSmem)
@@ -340,8 +333,6 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < tma_barriers(MODE, S); ++s) mbar_init(s_bar + s, 1);
-        if (SHB)
-            for (int s = 0; s < S; ++s) s_tick[s] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // kPark: pass 1's compensated beta_Q (hi, lo) lives in Tensor Memory (the lagging cursor has
@@ -365,8 +356,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     const int t3 = (n / R) * R;                        // first row of the (aligned) monitoring stream
     const int tid = threadIdx.x;
     const int wu = __shfl_sync(0xffffffffu, warp, 0);              // warp index, known warp-uniform
-    unsigned char* my_stage = SHB ? s_stage : s_stage + wu * S * SB;
-    uint64_t* full = SHB ? s_bar : s_bar + wu * S;
+    unsigned char* my_stage = s_stage + wu * S * SB;
+    uint64_t* full = s_bar + wu * S;
     const uint32_t stage_u32 = smem_u32(my_stage), bar_u32 = smem_u32(full);
 
     // ---- this warp's TMA issue cursor, kStages ahead of consumption ----------------------
@@ -380,13 +371,13 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     // (tile, stage); the first date of a stage comes from the schedule table.
     int64_t itile = blockIdx.x;
     int istage = 0;
-    int xw = (int)(itile * TILE) + (SHB ? 0 : wu * kWarpPx);   // x of the cursor's tile (slice)
-    constexpr uint32_t kBox = (uint32_t)(SHB ? kBoxBytes * NW : kBoxBytes);
-    auto issue_into = [&](int slot, bool really = true) {
+    int xw = (int)(itile * TILE) + wu * kWarpPx;       // x of the cursor's tile slice
+    constexpr uint32_t kBox = (uint32_t)kBoxBytes;
+    auto issue_into = [&](int slot) {
         if (itile >= n_tiles) return;
-        if (really) {
+        {
             const int r0 = s_rows[istage];
-            const uint32_t dst = stage_u32 + (uint32_t)(slot * SBX), bar = bar_u32 + (uint32_t)(slot * 8);
+            const uint32_t dst = stage_u32 + (uint32_t)(slot * SB), bar = bar_u32 + (uint32_t)(slot * 8);
             if (kLag && istage >= st1)
                 tma_box2_elect(dst, &prm.tmap, xw, r0, r0 - h, bar, 2 * kBox, kBox,    // + dates t-h
                                BWM_LAG_L2HINT < 2 || r0 + R <= N - h);                  // re-read as a lag row?
@@ -402,7 +393,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         }
     };
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap)) : "memory");
-    for (int s = 0; s < S; ++s) issue_into(s, !SHB || wu == 0);
+    for (int s = 0; s < S; ++s) issue_into(s);
 
     const int L = prm.ring_rows;
     const uint32_t tbase = MODE == kRingTmem
@@ -462,19 +453,11 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         if (!next_ready) mbar_wait(full + cur, ph);
         const int nc = cur + 1 == S ? 0 : cur + 1;
         next_ready = mbar_test(full + nc, nc == 0 ? ph ^ 1 : ph);
-        return reinterpret_cast<const float2*>(my_stage + cur * SBX) + (SHB ? wu * (kWarpPx / 2) : 0) + lane;
+        return reinterpret_cast<const float2*>(my_stage + cur * SB) + lane;
     };
     auto release = [&]() {
         __syncwarp();
-        bool mine = true;
-        if (SHB) {                                   // the last warp to release the slot re-arms it
-            uint32_t t = 0;
-            if (lane == 0) {
-                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(t) : "r"(smem_u32(s_tick + cur)) : "memory");
-            }
-            mine = (__shfl_sync(0xffffffffu, t, 0) % (uint32_t)NW) == (uint32_t)(NW - 1);
-        }
-        issue_into(cur, mine);                       // re-arm this slot kStages ahead
+        issue_into(cur);                             // re-arm this slot kStages ahead
         if (++cur == S) { cur = 0; ph ^= 1; }
     };
 
