@@ -166,8 +166,14 @@ int encode_map(CUtensorMap* map, const float* y, int64_t n_pixels, int n_obs, in
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
     const cuuint32_t box[2] = {(cuuint32_t)box_px, (cuuint32_t)bwm::kStageRows};
     const cuuint32_t estr[2] = {1, 1};
+    // L2 promotion of the box rows (A/B knob BWM_L2PROMO = 0 none, 1 64B, 2 128B, 3 256B; default 256B)
+    static const int promo = [] {
+        const char* e = std::getenv("BWM_L2PROMO");
+        const int v = e ? std::atoi(e) : 3;
+        return v < 0 || v > 3 ? 3 : v;
+    }();
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(y), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)promo,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err((int)cudaErrorInvalidValue, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return BWM_OK;
