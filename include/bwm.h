@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define BWM_ABI_VERSION 7
+#define BWM_ABI_VERSION 8
 
 /* error codes (negative); positive returns are cudaError_t values */
 #define BWM_OK 0
@@ -216,6 +216,7 @@ typedef struct bwm_plan_info_t {
     int32_t precise;          /* long horizon: float64 fitted values (LDG kernels); BWM_PRECISE=0/1   */
     int32_t mma;              /* lagging-cursor geometry: fitted values on the tensor cores (BWM_MMA)  */
     int64_t smem_mma;         /* dynamic shared memory per CTA of that kernel                         */
+    int32_t dyn_sched;        /* TMA kernel: dynamic per-warp slice scheduler (BWM_DYN=0: static)  (ABI 8) */
 } bwm_plan_info_t;
 
 int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info);

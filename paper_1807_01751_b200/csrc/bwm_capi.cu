@@ -310,6 +310,10 @@ struct bwm_plan {
     mutable int64_t* d_fix_list = nullptr;
     mutable unsigned int* d_fix_count = nullptr;
     mutable int64_t fix_cap = 0;
+    // TMA kernel: dynamic per-warp slice scheduler (two counters, zeroed here, reset by the
+    // kernel's last warp); plan scratch like the fixup list (BWM_DYN=0: static schedule)
+    unsigned int* d_sched = nullptr;
+    bool dyn = true;
     int bpm_tma_lean = 0;              // resident CTAs per SM of the LEAN TMA variant
     // lagging-cursor geometries: fitted values on the tensor cores (bwm_kernel_mma.cuh)
     bool use_mma = false;
@@ -357,6 +361,8 @@ static void plan_free_tables(bwm_plan* plan) {
     cudaFree(plan->d_wtd);
     cudaFree(plan->d_fix_list);
     cudaFree(plan->d_fix_count);
+    cudaFree(plan->d_sched);
+    plan->d_sched = nullptr;
     cudaFree(plan->d_xx);
     cudaFree(plan->d_gfull);
     cudaFree(plan->d_ring);
@@ -616,6 +622,17 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         if (e0 != cudaSuccess) {
             delete plan;
             return set_err((int)e0, "cudaEventCreate: %s", cudaGetErrorString(e0));
+        }
+        const char* dyn_env = getenv("BWM_DYN");
+        plan->dyn = !(dyn_env && std::strcmp(dyn_env, "0") == 0);
+        if (plan->dyn && dims->nan_mode != BWM_NAN_MASK) {
+            e0 = cudaMalloc(&plan->d_sched, 2 * sizeof(unsigned int));
+            if (e0 == cudaSuccess) e0 = cudaMemset(plan->d_sched, 0, 2 * sizeof(unsigned int));
+            if (e0 != cudaSuccess) {
+                plan_free_tables(plan);
+                delete plan;
+                return set_err((int)e0, "scheduler counters: %s", cudaGetErrorString(e0));
+            }
         }
     }
     if (dims->nan_mode == BWM_NAN_MASK) return plan_create_masked(plan, tb, max_optin, out_plan);
@@ -924,7 +941,16 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     int launched = 0;
     // float64 fixup list for ill-conditioned pixels (fill mode, float32 kernels)
     const bool fixup = !plan->masked && !plan->precise && plan->fix_ratio > 0.f && plan->d_xtd;
-    const bool uses_scratch = fixup || (plan->masked && !plan->precise && plan->mbig);
+    // dynamic slice scheduler of the TMA kernel: the cursor must enter a slice S stages before
+    // consumption leaves the previous one (tile_stages > S, bwm_kernel_tma.cuh)
+    const bool dyn = [&] {
+        if (plan->masked || !plan->d_sched || plan->use_mma || plan->tring.mode < 0) return false;
+        const int R = bwm::kStageRows, n = d.n_hist, N = d.n_obs;
+        const int t3 = (n / R) * R;
+        const int tile_stages = (n + R - 1) / R + (N - t3 + R - 1) / R;
+        return tile_stages > bwm::stages_for(plan->tring.mode);
+    }();
+    const bool uses_scratch = fixup || dyn || (plan->masked && !plan->precise && plan->mbig);
     std::unique_lock<std::mutex> scratch_lock(plan->scratch_mu, std::defer_lock);
     if (uses_scratch) {
         scratch_lock.lock();
@@ -1032,6 +1058,7 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
         if (kind == kTma) {
             int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y, bwm::kWarpPx);
             if (rc) return rc;
+            kp.sched = dyn ? plan->d_sched : nullptr;
         }
         fn<<<(unsigned)grid, threads_of(kind, plan->tring.mode), sm, st>>>(kp);
         cudaError_t e = cudaGetLastError();
@@ -1484,6 +1511,7 @@ int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {
     info->precise = plan->precise ? 1 : 0;
     info->mma = plan->use_mma ? 1 : 0;
     info->smem_mma = plan->smem_mma;
+    info->dyn_sched = plan->d_sched ? 1 : 0;
     return BWM_OK;
 }
 

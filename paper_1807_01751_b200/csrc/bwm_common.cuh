@@ -78,6 +78,9 @@ struct KParams {
     const float* wt;            // [N][sp] rows t < n: q_t (Q^T); rows t >= n: S_t (column 0 = 0)
     const double* wtd;          // the same table in float64 (precise mode), or nullptr
     double s0;                  // h * z[0]
+    // TMA kernel: dynamic per-warp slice scheduler ([0] claim counter, [1] finished warps; the
+    // last warp to finish resets both, so every launch starts from 0) — nullptr: static schedule
+    unsigned int* sched;
 };
 
 // append pixel `px` (launch-relative) to the fixup list when its history fit is ill-conditioned:

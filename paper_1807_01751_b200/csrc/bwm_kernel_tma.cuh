@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     __syncthreads();
     if (kTmem) tmem_fence_after();
 
-    const int64_t n_tiles = prm.n_pixels / TILE;       // host guarantees whole tiles
+    // host guarantees whole tiles (TILE = NW slices of 64 px)
     const int64_t ld = prm.ld_y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // initial window: dates [n-h, n) (window 0 of mosum.py:59 is [n-h+1, n]; the first
@@ -368,13 +368,27 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     const int st1 = (n + R - 1) / R;
     const int tile_stages = st1 + (N - t3 + R - 1) / R;
     // The slot re-armed at a release is the one just consumed, so the issue cursor needs only
-    // (tile, stage); the first date of a stage comes from the schedule table.
-    int64_t itile = blockIdx.x;
+    // (slice, stage); the first date of a stage comes from the schedule table.
+    // Work unit: a 64-px warp SLICE (warps are independent pipelines).  Static schedule: warp
+    // w of CTA b takes slices b NW + w, then strides by the grid's warp count.  Dynamic
+    // (prm.sched): the first slice is static, every later one is claimed from a global counter
+    // one slice AHEAD (the atomic's latency hides behind a whole slice), so warps that run
+    // ahead — free-running warps drift apart, and SMs differ — take more slices instead of
+    // idling at the end of the kernel.  The cursor moves to the next slice S stages before
+    // consumption does (host: tile_stages > S), so one `pending` register carries the slice
+    // consumption takes next.
+    const int64_t n_slices = prm.n_pixels / kWarpPx;
+    const int64_t n_warps = (int64_t)gridDim.x * NW;
+    const bool dyn = prm.sched != nullptr;
+    int64_t islice = (int64_t)blockIdx.x * NW + wu;
+    int64_t pending = islice;
+    unsigned int pre = 0;                             // lane 0: the pre-claimed next slice (dynamic)
+    if (dyn && lane == 0) pre = atomicAdd(prm.sched, 1u);
     int istage = 0;
-    int xw = (int)(itile * TILE) + wu * kWarpPx;       // x of the cursor's tile slice
+    int xw = (int)(islice * kWarpPx);                 // x of the cursor's slice
     constexpr uint32_t kBox = (uint32_t)kBoxBytes;
     auto issue_into = [&](int slot) {
-        if (itile >= n_tiles) return;
+        if (islice >= n_slices) return;
         {
             const int r0 = s_rows[istage];
             const uint32_t dst = stage_u32 + (uint32_t)(slot * SB), bar = bar_u32 + (uint32_t)(slot * 8);
@@ -388,8 +402,22 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         }
         if (++istage == tile_stages) {
             istage = 0;
-            itile += gridDim.x;
-            xw += (int)gridDim.x * TILE;
+            if (dyn) {
+                islice = n_warps + (int64_t)__shfl_sync(0xffffffffu, pre, 0);
+                if (islice < n_slices) {
+                    if (lane == 0) pre = atomicAdd(prm.sched, 1u);
+                } else if (lane == 0) {
+                    // this warp's last claim; the last warp of the launch resets the scheduler
+                    if (atomicAdd(prm.sched + 1, 1u) == (unsigned int)(n_warps - 1)) {
+                        atomicExch(prm.sched, 0u);
+                        atomicExch(prm.sched + 1, 0u);
+                    }
+                }
+            } else {
+                islice += n_warps;
+            }
+            pending = islice;
+            xw = (int)(islice * kWarpPx);
         }
     };
     if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&prm.tmap)) : "memory");
@@ -461,8 +489,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         if (++cur == S) { cur = 0; ph ^= 1; }
     };
 
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int64_t px0 = tile * TILE + 2 * tid;
+    for (int64_t slice = pending; slice < n_slices; slice = dyn ? pending : slice + n_warps) {
+        const int64_t px0 = slice * kWarpPx + 2 * lane;
         const float* yp = prm.y + px0;
 
         // ---- pass 1: beta_Q and ||y - c||^2 (+ pass 0 on the first stage) ---------------

@@ -42,7 +42,7 @@ def test_abi_version_and_error_string():
     from paper_1807_01751_b200 import _lib
 
     lib = _lib.load()
-    assert lib.bwm_abi_version() == _lib.ABI_VERSION == 7
+    assert lib.bwm_abi_version() == _lib.ABI_VERSION == 8
     assert isinstance(lib.bwm_last_error(), bytes)
 
 

@@ -137,3 +137,25 @@ def test_fullsize_masked_shift_and_shards():
     hi = _maps(plan.run_device(y[:, cut:], pixel_offset=cut))
     for a, b, c in zip(base, lo, hi):
         assert np.array_equal(a, np.concatenate([b, c]))
+
+
+@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
+def test_fullsize_dynamic_schedule(name, monkeypatch):
+    """The TMA kernel's dynamic per-warp slice scheduler (default) hands 64-px slices to
+    whichever warp asks first, so a pixel's slice lands on a different warp, CTA and SM from
+    run to run: the maps must equal the static schedule's bit for bit, and repeated calls on
+    one plan (the scheduler's counters reset themselves at the end of every launch) must too."""
+    from paper_1807_01751_b200.device import DevicePlan
+    from paper_1807_01751_b200.model import TimeAxis
+
+    w, t, plan, y = _setup(name)
+    assert plan.info()["dyn_sched"] == 1
+    runs = [_maps(plan.run_device(y)) for _ in range(3)]
+    monkeypatch.setenv("BWM_DYN", "0")
+    static = DevicePlan(TimeAxis(t), w.freq, w.harmonics, w.n_hist, w.bandwidth, w.crit, "cuda")
+    monkeypatch.delenv("BWM_DYN")
+    assert static.info()["dyn_sched"] == 0
+    ref = _maps(static.run_device(y))
+    for got in runs:
+        for a, b in zip(ref, got):
+            assert np.array_equal(a, b)

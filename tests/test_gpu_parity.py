@@ -140,6 +140,31 @@ def test_kernel_variants_bit_identical(name, monkeypatch):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("name", ["c1", "c4_tile", "lag_h100", "edges_h10_k2"])
+def test_dynamic_schedule_bit_identical(name, monkeypatch):
+    """The TMA kernel's dynamic slice scheduler (default) against the static schedule
+    (BWM_DYN=0), and back-to-back calls on one plan (the counters reset in-kernel): same bits."""
+    import torch
+
+    from paper_1807_01751_b200.device import DevicePlan
+    from paper_1807_01751_b200.model import TimeAxis
+
+    case = load(name)
+    y = torch.as_tensor(case.y, device="cuda")
+    dyn = _plan(case)
+    runs = [_maps(dyn.run_device(y, beta=True, mean=True)) for _ in range(3)]
+    runs.append(_maps(dyn.run_device(y))[:3] + [None, None])           # LEAN variant
+    monkeypatch.setenv("BWM_DYN", "0")
+    static = DevicePlan(TimeAxis(case.t), case.freq, case.k, case.n, case.h, case.crit, "cuda")
+    monkeypatch.delenv("BWM_DYN")
+    assert static.info()["dyn_sched"] == 0
+    ref = _maps(static.run_device(y, beta=True, mean=True))
+    for got in runs:
+        for a, b in zip(ref, got):
+            if b is not None:
+                assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("P", [3000, 1024 + 2, 77])
 def test_lagging_cursor_ragged_tail(P):
     """c4_tile (h = 250: the 16-warp lagging-cursor TMA kernel, 1,024-px tiles) cut to P pixels:

