@@ -73,7 +73,7 @@ class PlanInfo(C.Structure):
         ("ctas_per_sm_ldg", C.c_int32), ("occupancy_tma", C.c_int32), ("force_ldg", C.c_int32),
         ("nan_mode", C.c_int32), ("masked_global", C.c_int32), ("ctas_per_sm_masked", C.c_int32),
         ("smem_masked", C.c_int64), ("const_bound", C.c_int32), ("ctas_per_sm_tma_lean", C.c_int32),
-        ("precise", C.c_int32), ("mma", C.c_int32), ("smem_mma", C.c_int64), ("dyn_sched", C.c_int32),
+        ("precise", C.c_int32), ("mma", C.c_int32), ("smem_mma", C.c_int64), ("dyn_sched", C.c_int32), ("tall_stages", C.c_int32),
     ]
 
 

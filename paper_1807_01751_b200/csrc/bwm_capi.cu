@@ -159,12 +159,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D map of a time-major float32 block: dim0 = pixels (contiguous), dim1 = dates (stride ld)
-int encode_map(CUtensorMap* map, const float* y, int64_t n_pixels, int n_obs, int64_t ld, int box_px = bwm::kWarpPx) {
+int encode_map(CUtensorMap* map, const float* y, int64_t n_pixels, int n_obs, int64_t ld, int box_px = bwm::kWarpPx,
+               int box_rows = bwm::kStageRows) {
     auto fn = encode_fn();
     if (!fn) return set_err((int)cudaErrorNotSupported, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[2] = {(cuuint64_t)n_pixels, (cuuint64_t)n_obs};
     const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)box_px, (cuuint32_t)bwm::kStageRows};
+    const cuuint32_t box[2] = {(cuuint32_t)box_px, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     // L2 promotion of the box rows (A/B knob BWM_L2PROMO = 0 none, 1 64B, 2 128B, 3 256B; default 256B)
     static const int promo = [] {
@@ -314,6 +315,12 @@ struct bwm_plan {
     // kernel's last warp); plan scratch like the fixup list (BWM_DYN=0: static schedule)
     unsigned int* d_sched = nullptr;
     bool dyn = true;
+    // TALL variant of the LEAN TMEM-ring kernel (16-date stages, bwm_kernel_tma.cuh): used for
+    // LEAN launches when its ring needs the same Tensor Memory and CTAs per SM (BWM_TALL=0: off)
+    bool tall = false;
+    TmaRing tring_tall{};
+    int64_t smem_tall = 0;
+    int bpm_tall = 0;
     int bpm_tma_lean = 0;              // resident CTAs per SM of the LEAN TMA variant
     // lagging-cursor geometries: fitted values on the tensor cores (bwm_kernel_mma.cuh)
     bool use_mma = false;
@@ -851,6 +858,31 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
             plan->bpm_tma_lean = std::max(nb, 1);
         }
     }
+    {
+        const char* tall_env = getenv("BWM_TALL");
+        const bool want = !(tall_env && std::strcmp(tall_env, "0") == 0);
+        constexpr int RT = bwm::kTallRows;
+        if (want && bwm::kStageRows == 8 && plan->tring.mode == (int)bwm::kRingTmem && plan->smem_tma > 0 &&
+            plan->const_bound && h >= RT) {
+            const int L = ((h + RT - 1) / RT) * RT;
+            const int need = 2 * (L + RT);
+            int cols = 32;
+            while (cols < need) cols *= 2;
+            if (need <= tmem_cols_max() && cols == plan->tring.cols) {
+                const int64_t sm = plan->smem_tma - bwm::tma_stage_region(bwm::kRingTmem, bwm::kStages) +
+                                   (int64_t)bwm::tma_warps(bwm::kRingTmem) * BWM_STAGES_TALL * RT * bwm::kWarpPx * 4;
+                int nb = 0;
+                if ((e = setup(pick(p, kTma, bwm::kRingTmem | bwm::kTmaLean | bwm::kTmaTall), kTma, sm, &nb)) != cudaSuccess)
+                    return fail(e, "kernel setup (tall)");
+                if (nb >= plan->bpm_tma_lean) {
+                    plan->tall = true;
+                    plan->tring_tall = {(int)bwm::kRingTmem, L, cols};
+                    plan->smem_tall = sm;
+                    plan->bpm_tall = nb;
+                }
+            }
+        }
+    }
     *out_plan = plan;
     return BWM_OK;
 }
@@ -943,14 +975,16 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
     const bool fixup = !plan->masked && !plan->precise && plan->fix_ratio > 0.f && plan->d_xtd;
     // dynamic slice scheduler of the TMA kernel: the cursor must enter a slice S stages before
     // consumption leaves the previous one (tile_stages > S, bwm_kernel_tma.cuh)
-    const bool dyn = [&] {
+    auto dyn_for = [&](int R, int S) {
         if (plan->masked || !plan->d_sched || plan->use_mma || plan->tring.mode < 0) return false;
-        const int R = bwm::kStageRows, n = d.n_hist, N = d.n_obs;
+        const int n = d.n_hist, N = d.n_obs;
         const int t3 = (n / R) * R;
         const int tile_stages = (n + R - 1) / R + (N - t3 + R - 1) / R;
-        return tile_stages > bwm::stages_for(plan->tring.mode);
-    }();
-    const bool uses_scratch = fixup || dyn || (plan->masked && !plan->precise && plan->mbig);
+        return tile_stages > S;
+    };
+    const bool dyn = dyn_for(bwm::kStageRows, bwm::stages_for(plan->tring.mode));
+    const bool dyn_tall = plan->tall && dyn_for(bwm::kTallRows, BWM_STAGES_TALL);
+    const bool uses_scratch = fixup || dyn || dyn_tall || (plan->masked && !plan->precise && plan->mbig);
     std::unique_lock<std::mutex> scratch_lock(plan->scratch_mu, std::defer_lock);
     if (uses_scratch) {
         scratch_lock.lock();
@@ -1048,17 +1082,22 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
             ++launched;
             continue;
         }
-        KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode | (lean ? bwm::kTmaLean : 0)
+        const bool tall = lean && plan->tall;
+        KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode | (lean ? bwm::kTmaLean : 0) | (tall ? bwm::kTmaTall : 0)
                                                           : (plan->ring ? 0 : (int)bwm::kRingLag));
         const int64_t tile = kind == kTma ? bwm::tma_tile(plan->tring.mode) : bwm::kTile;
         const int64_t tiles = (cnt + tile - 1) / tile;
-        const int bpm = lean ? plan->bpm_tma_lean : plan->blocks_per_sm[kind];
+        const int bpm = tall ? plan->bpm_tall : lean ? plan->bpm_tma_lean : plan->blocks_per_sm[kind];
         const int64_t grid = std::min<int64_t>(tiles, (int64_t)plan->sms * bpm);
-        const size_t sm = (size_t)(kind == kTma ? plan->smem_tma : plan->smem);
+        const size_t sm = (size_t)(tall ? plan->smem_tall : kind == kTma ? plan->smem_tma : plan->smem);
         if (kind == kTma) {
-            int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y, bwm::kWarpPx);
+            int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y, bwm::kWarpPx, tall ? bwm::kTallRows : bwm::kStageRows);
             if (rc) return rc;
-            kp.sched = dyn ? plan->d_sched : nullptr;
+            kp.sched = (tall ? dyn_tall : dyn) ? plan->d_sched : nullptr;
+            if (tall) {
+                kp.ring_rows = plan->tring_tall.rows;
+                kp.tmem_cols = plan->tring_tall.cols;
+            }
         }
         fn<<<(unsigned)grid, threads_of(kind, plan->tring.mode), sm, st>>>(kp);
         cudaError_t e = cudaGetLastError();
@@ -1512,6 +1551,7 @@ int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {
     info->mma = plan->use_mma ? 1 : 0;
     info->smem_mma = plan->smem_mma;
     info->dyn_sched = plan->d_sched ? 1 : 0;
+    info->tall_stages = plan->tall ? 1 : 0;
     return BWM_OK;
 }
 

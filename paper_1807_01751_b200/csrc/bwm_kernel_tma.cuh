@@ -59,10 +59,11 @@ namespace bwm {
 #endif
 constexpr int kStageRows = BWM_STAGE_ROWS;      // dates per stage (multiple of 8)
 #ifndef BWM_LAG_L2HINT
-#define BWM_LAG_L2HINT 0   // L2 evict_last/evict_first hints on the lag boxes: measured 8.21 vs 8.18 ms at C4, off
-#endif                     // 2: also pass-1 rows and never-re-read lead rows (evict_first)
+#define BWM_LAG_L2HINT 2   // L2 evict_last/evict_first hints on the lagging cursor's boxes (1: lead keep / lag drop;
+#endif                     // 2: also pass-1 rows and never-re-read lead rows evict_first).  Static schedule: 2% slower;
+                           // with the dynamic slice scheduler C4 is near DRAM-bound and mode 2 at keep 0.5 is 1% faster
 #ifndef BWM_LAG_KEEP
-#define BWM_LAG_KEEP 1.0   // fraction of a kept box's lines that get evict_last (createpolicy.fractional)
+#define BWM_LAG_KEEP 0.5   // fraction of a kept box's lines that get evict_last (createpolicy.fractional)
 #endif
 #define BWM_STR2(x) #x
 #define BWM_STR(x) BWM_STR2(x)
@@ -90,6 +91,10 @@ constexpr bool kMirror = BWM_RING_MIRROR != 0;
 #ifndef BWM_STAGES_LAGT
 #define BWM_STAGES_LAGT 2
 #endif
+#ifndef BWM_STAGES_TALL
+#define BWM_STAGES_TALL 2  // TALL variant (16-date stages, TMEM ring, LEAN): stages per warp (C2: 2 beat 3)
+#endif
+constexpr int kTallRows = 16;
 __host__ __device__ constexpr int stages_for(int mode) {
     return mode == 2 /* kRingLag */ ? BWM_STAGES_LAG : mode == 3 /* kRingLagT */ ? BWM_STAGES_LAGT : kStages;
 }
@@ -291,15 +296,19 @@ __host__ __device__ constexpr int tma_barriers(int mode, int stages) {
 // period (b_j = lambda for every j: log_plus((n+1+j)/n) = 1 while (n+1+j)/n <= e, which holds
 // for all BASELINE geometries, N/n = 2) — the per-date boundary product, mean accumulation
 // and output branch drop out of the MOSUM loop.  Results are bit-identical to !LEAN.
-template <int NP, int MODE, bool LEAN>
+// RR: dates per stage — kStageRows (8), or kTallRows (16) for the TALL variant of the TMEM-ring
+// LEAN kernel (half the TMA boxes, barriers and stage bookkeeping per date; the host picks it
+// when its ring needs no more Tensor Memory than the 8-date one, e.g. C2: 5% faster).
+template <int NP, int MODE, bool LEAN, int RR = kStageRows>
 __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     monitor_kernel_tma(const __grid_constant__ KParams prm) {
     static_assert(MODE == kRingTmem || MODE == kRingLag || MODE == kRingLagT, "TMA kernel: TMEM ring or lagging cursor");
     constexpr bool kLag = MODE == kRingLag || MODE == kRingLagT;
     constexpr int SP = Coefs<NP>::SP;
-    constexpr int R = kStageRows;
-    constexpr int S = stages_for(MODE);
-    constexpr int64_t SB = tma_stage_bytes(MODE);
+    constexpr int R = RR;
+    static_assert(RR == kStageRows || (RR == kTallRows && MODE == kRingTmem), "TALL: TMEM ring only");
+    constexpr int S = RR == kStageRows ? stages_for(MODE) : BWM_STAGES_TALL;
+    constexpr int64_t SB = (int64_t)R * kWarpPx * 4 * (kLag ? 2 : 1);
     constexpr int NW = tma_warps(MODE), NT = tma_threads(MODE), TILE = tma_tile(MODE);
     constexpr int ROWF2 = kWarpPx / 2;                   // float2 per staged row
     static_assert(MODE != kRingTmem || NW % 4 == 0, "TMEM ring: warps in whole lane quarters");
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     // kRingLag (long series): the table stays in global memory and is read through L1 (uniform
     // addresses, broadcast).
     constexpr bool kTblSmem = MODE != kRingLag;
-    float* s_tbl = reinterpret_cast<float*>(smem_raw + tma_stage_region(MODE, S));
+    float* s_tbl = reinterpret_cast<float*>(smem_raw + (int64_t)NW * S * SB);
     const float* s_xt = kTblSmem ? s_tbl : prm.wt;
     const float* s_mt = s_xt;
     float* s_bd = s_tbl + (kTblSmem ? N * SP : 0);                       // [NA] bound by row t (t >= n)
@@ -326,10 +335,10 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     {
         // the per-tile stage schedule (identical for every tile): pass 1 [0, n), pass 3
         // [8 floor(n/8), N), R dates per stage
-        const int t3_ = (n / kStageRows) * kStageRows;
-        const int a = (n + kStageRows - 1) / kStageRows;
-        const int c = a + (N - t3_ + kStageRows - 1) / kStageRows;
-        for (int i = threadIdx.x; i < c; i += NT) s_rows[i] = i < a ? i * kStageRows : t3_ + (i - a) * kStageRows;
+        const int t3_ = (n / R) * R;
+        const int a = (n + R - 1) / R;
+        const int c = a + (N - t3_ + R - 1) / R;
+        for (int i = threadIdx.x; i < c; i += NT) s_rows[i] = i < a ? i * R : t3_ + (i - a) * R;
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < tma_barriers(MODE, S); ++s) mbar_init(s_bar + s, 1);
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     if (dyn && lane == 0) pre = atomicAdd(prm.sched, 1u);
     int istage = 0;
     int xw = (int)(islice * kWarpPx);                 // x of the cursor's slice
-    constexpr uint32_t kBox = (uint32_t)kBoxBytes;
+    constexpr uint32_t kBox = (uint32_t)(R * kWarpPx * 4);
     auto issue_into = [&](int slot) {
         if (islice >= n_slices) return;
         {

@@ -163,6 +163,15 @@ def test_dynamic_schedule_bit_identical(name, monkeypatch):
         for a, b in zip(ref, got):
             if b is not None:
                 assert np.array_equal(a, b)
+    # the LEAN launch's 16-date-stage (TALL) variant against the 8-date kernel
+    monkeypatch.setenv("BWM_TALL", "0")
+    short = DevicePlan(TimeAxis(case.t), case.freq, case.k, case.n, case.h, case.crit, "cuda")
+    monkeypatch.delenv("BWM_TALL")
+    assert short.info()["tall_stages"] == 0
+    if name in ("c1", "c4_tile"):
+        assert dyn.info()["tall_stages"] == (1 if name == "c1" else 0)
+    for a, b in zip(_maps(short.run_device(y))[:3], runs[-1][:3]):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("P", [3000, 1024 + 2, 77])
