@@ -217,7 +217,7 @@ typedef struct bwm_plan_info_t {
     int32_t mma;              /* lagging-cursor geometry: fitted values on the tensor cores (BWM_MMA)  */
     int64_t smem_mma;         /* dynamic shared memory per CTA of that kernel                         */
     int32_t dyn_sched;        /* TMA kernel: dynamic per-warp slice scheduler (BWM_DYN=0: static)  (ABI 8) */
-    int32_t tall_stages;      /* LEAN TMEM-ring launches use 16-date stages (BWM_TALL=0: off)       (ABI 8) */
+    int32_t tall_stages;      /* LEAN TMEM-ring launches use 16-date stages: 1 (2: ring without mirror rows); BWM_TALL=0: off (ABI 8) */
 } bwm_plan_info_t;
 
 int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info);

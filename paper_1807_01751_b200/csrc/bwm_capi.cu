@@ -318,6 +318,7 @@ struct bwm_plan {
     // TALL variant of the LEAN TMEM-ring kernel (16-date stages, bwm_kernel_tma.cuh): used for
     // LEAN launches when its ring needs the same Tensor Memory and CTAs per SM (BWM_TALL=0: off)
     bool tall = false;
+    bool tall_nomirror = false;        // the TALL ring without mirror rows (fits where 16 mirror rows would not)
     TmaRing tring_tall{};
     int64_t smem_tall = 0;
     int bpm_tall = 0;
@@ -865,17 +866,23 @@ int bwm_plan_create(const bwm_dims* dims, const bwm_tables* tb, int device, bwm_
         if (want && bwm::kStageRows == 8 && plan->tring.mode == (int)bwm::kRingTmem && plan->smem_tma > 0 &&
             plan->const_bound && h >= RT) {
             const int L = ((h + RT - 1) / RT) * RT;
-            const int need = 2 * (L + RT);
-            int cols = 32;
-            while (cols < need) cols *= 2;
-            if (need <= tmem_cols_max() && cols == plan->tring.cols) {
+            auto pow2 = [](int need) { int c = 32; while (c < need) c *= 2; return c; };
+            const char* nm_env = getenv("BWM_TALL_NOMIRROR");       // A/B: 0 never, 1 whenever mirrors do not fit
+            const bool nm_ok = !(nm_env && std::strcmp(nm_env, "0") == 0);
+            const bool mir = pow2(2 * (L + RT)) == plan->tring.cols;
+            const bool nomir = !mir && nm_ok && pow2(2 * L) == plan->tring.cols;
+            const int need = 2 * (L + (mir ? RT : 0));
+            const int cols = pow2(need);
+            if ((mir || nomir) && need <= tmem_cols_max()) {
                 const int64_t sm = plan->smem_tma - bwm::tma_stage_region(bwm::kRingTmem, bwm::kStages) +
                                    (int64_t)bwm::tma_warps(bwm::kRingTmem) * BWM_STAGES_TALL * RT * bwm::kWarpPx * 4;
                 int nb = 0;
-                if ((e = setup(pick(p, kTma, bwm::kRingTmem | bwm::kTmaLean | bwm::kTmaTall), kTma, sm, &nb)) != cudaSuccess)
+                const int tmode = bwm::kRingTmem | bwm::kTmaLean | bwm::kTmaTall | (nomir ? bwm::kTmaNoMirror : 0);
+                if ((e = setup(pick(p, kTma, tmode), kTma, sm, &nb)) != cudaSuccess)
                     return fail(e, "kernel setup (tall)");
                 if (nb >= plan->bpm_tma_lean) {
                     plan->tall = true;
+                    plan->tall_nomirror = nomir;
                     plan->tring_tall = {(int)bwm::kRingTmem, L, cols};
                     plan->smem_tall = sm;
                     plan->bpm_tall = nb;
@@ -1083,7 +1090,8 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
             continue;
         }
         const bool tall = lean && plan->tall;
-        KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode | (lean ? bwm::kTmaLean : 0) | (tall ? bwm::kTmaTall : 0)
+        KernelFn fn = pick(d.n_params, kind, kind == kTma ? plan->tring.mode | (lean ? bwm::kTmaLean : 0) | (tall ? bwm::kTmaTall : 0) |
+                                                                (tall && plan->tall_nomirror ? bwm::kTmaNoMirror : 0)
                                                           : (plan->ring ? 0 : (int)bwm::kRingLag));
         const int64_t tile = kind == kTma ? bwm::tma_tile(plan->tring.mode) : bwm::kTile;
         const int64_t tiles = (cnt + tile - 1) / tile;
@@ -1551,7 +1559,7 @@ int bwm_plan_info(const bwm_plan* plan, bwm_plan_info_t* info) {
     info->mma = plan->use_mma ? 1 : 0;
     info->smem_mma = plan->smem_mma;
     info->dyn_sched = plan->d_sched ? 1 : 0;
-    info->tall_stages = plan->tall ? 1 : 0;
+    info->tall_stages = plan->tall ? (plan->tall_nomirror ? 2 : 1) : 0;
     return BWM_OK;
 }
 

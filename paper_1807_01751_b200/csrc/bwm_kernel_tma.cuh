@@ -299,7 +299,10 @@ __host__ __device__ constexpr int tma_barriers(int mode, int stages) {
 // RR: dates per stage — kStageRows (8), or kTallRows (16) for the TALL variant of the TMEM-ring
 // LEAN kernel (half the TMA boxes, barriers and stage bookkeeping per date; the host picks it
 // when its ring needs no more Tensor Memory than the 8-date one, e.g. C2: 5% faster).
-template <int NP, int MODE, bool LEAN, int RR = kStageRows>
+// MIR: R mirror rows after the TMEM ring (no wrapped lag loads); a TALL ring that would need more
+// Tensor Memory with them (C5: 64 + 16 rows) runs without (MIR = false: a stage whose lagged run
+// wraps loads it row by row).
+template <int NP, int MODE, bool LEAN, int RR = kStageRows, bool MIR = kMirror>
 __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     monitor_kernel_tma(const __grid_constant__ KParams prm) {
     static_assert(MODE == kRingTmem || MODE == kRingLag || MODE == kRingLagT, "TMA kernel: TMEM ring or lagging cursor");
@@ -444,7 +447,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     const int q_t3 = MODE == kRingTmem ? t3 % L : 0, q_t3h = MODE == kRingTmem ? ((t3 - h) % L + L) % L : 0;
     auto ring_put_row = [&](int q, float2 v) {                             // q < L (+ mirror)
         tmem_st2(tcol(q), v);
-        if (kMirror && q < R) tmem_st2(tcol(q + L), v);
+        if (MIR && q < R) tmem_st2(tcol(q + L), v);
     };
     auto ring_ld2 = [&](int q, float2& v) {                                // no wait
         uint32_t a, b;
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     // run never wraps — R/8 tcgen05.ld.x16
     auto ring_load = [&](int q0, float2 (&v)[R]) {
         tmem_wait_st();
-        if (kMirror || q0 + R <= L) {
+        if (MIR || q0 + R <= L) {
 #pragma unroll
             for (int c8 = 0; c8 < R / 8; ++c8)
                 tmem_ld16(tcol(q0 + 8 * c8), *reinterpret_cast<float2(*)[8]>(&v[8 * c8]));
@@ -475,7 +478,7 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
 #pragma unroll
         for (int c8 = 0; c8 < R / 8; ++c8)
             tmem_st16(tcol(q0 + 8 * c8), *reinterpret_cast<const float2(*)[8]>(&v[8 * c8]));
-        if (kMirror && q0 == 0) {                            // rows 0..R-1: their mirror too
+        if (MIR && q0 == 0) {                                // rows 0..R-1: their mirror too
 #pragma unroll
             for (int c8 = 0; c8 < R / 8; ++c8)
                 tmem_st16(tcol(L + 8 * c8), *reinterpret_cast<const float2(*)[8]>(&v[8 * c8]));

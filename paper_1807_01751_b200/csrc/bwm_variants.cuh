@@ -10,6 +10,7 @@ enum Kind { kLdgFast = 0, kLdgSafe = 1, kTma = 2 };
 using KernelFn = void (*)(const KParams);
 constexpr int kTmaLean = 0x10;   // pick(): OR into the TMA ring mode for the LEAN variant
 constexpr int kTmaTall = 0x20;   // pick(): with kRingTmem | kTmaLean, the 16-date-stage (TALL) variant
+constexpr int kTmaNoMirror = 0x40;   // with kTmaTall: the ring without mirror rows
 }  // namespace bwm
 
 // Defines bwm::KernelFn bwm_pick_p<NP>(int kind, int mode) in the including TU.
@@ -26,7 +27,9 @@ constexpr int kTmaTall = 0x20;   // pick(): with kRingTmem | kTmaLean, the 16-da
                 return ring ? bwm::monitor_kernel_ldg<NP, true, true> : bwm::monitor_kernel_ldg<NP, true, false>;   \
             default:                                                                             \
                 if ((mode & bwm::kTmaTall) && (mode & 0xF) == bwm::kRingTmem)                    \
-                    return bwm::monitor_kernel_tma<NP, bwm::kRingTmem, true, bwm::kTallRows>;      \
+                    return (mode & bwm::kTmaNoMirror)                                            \
+                               ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem, true, bwm::kTallRows, false> \
+                               : bwm::monitor_kernel_tma<NP, bwm::kRingTmem, true, bwm::kTallRows, true>; \
                 if (mode & bwm::kTmaLean)                                                        \
                     return (mode & 0xF) == bwm::kRingTmem  ? bwm::monitor_kernel_tma<NP, bwm::kRingTmem, true>  \
                            : (mode & 0xF) == bwm::kRingLagT ? bwm::monitor_kernel_tma<NP, bwm::kRingLagT, true> \

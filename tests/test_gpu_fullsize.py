@@ -159,8 +159,9 @@ def test_fullsize_dynamic_schedule(name, monkeypatch):
     for got in runs:
         for a, b in zip(ref, got):
             assert np.array_equal(a, b)
-    # C2 runs its LEAN launches on the 16-date-stage (TALL) variant: same bits as 8-date stages
-    assert plan.info()["tall_stages"] == (1 if name == "C2" else 0)
+    # C2 runs its LEAN launches on the 16-date-stage (TALL) variant, C5 on the TALL variant without
+    # ring mirror rows: same bits as 8-date stages
+    assert plan.info()["tall_stages"] == {"C2": 1, "C4": 0, "C5": 2}[name]
     monkeypatch.setenv("BWM_TALL", "0")
     short = DevicePlan(TimeAxis(t), w.freq, w.harmonics, w.n_hist, w.bandwidth, w.crit, "cuda")
     monkeypatch.delenv("BWM_TALL")

@@ -140,7 +140,7 @@ def test_kernel_variants_bit_identical(name, monkeypatch):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("name", ["c1", "c4_tile", "lag_h100", "edges_h10_k2"])
+@pytest.mark.parametrize("name", ["c1", "c4_tile", "lag_h100", "edges_h10_k2", "c5_tile", "three_pixels"])
 def test_dynamic_schedule_bit_identical(name, monkeypatch):
     """The TMA kernel's dynamic slice scheduler (default) against the static schedule
     (BWM_DYN=0), and back-to-back calls on one plan (the counters reset in-kernel): same bits."""
@@ -168,8 +168,11 @@ def test_dynamic_schedule_bit_identical(name, monkeypatch):
     short = DevicePlan(TimeAxis(case.t), case.freq, case.k, case.n, case.h, case.crit, "cuda")
     monkeypatch.delenv("BWM_TALL")
     assert short.info()["tall_stages"] == 0
-    if name in ("c1", "c4_tile"):
-        assert dyn.info()["tall_stages"] == (1 if name == "c1" else 0)
+    # 16-date stages: c1 with mirror rows (1), c5_tile without (2: 64 + 16 rows would double the
+    # TMEM allocation), the lagging cursor never
+    expect = {"c1": 1, "c4_tile": 0, "c5_tile": 2, "lag_h100": 1}
+    if name in expect:
+        assert dyn.info()["tall_stages"] == expect[name]
     for a, b in zip(_maps(short.run_device(y))[:3], runs[-1][:3]):
         assert np.array_equal(a, b)
 
