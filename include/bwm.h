@@ -129,8 +129,9 @@ void bwm_plan_destroy(bwm_plan* plan);
  * whose ||y - c||^2 / RSS exceeds 300 (BWM_FIX_RATIO) are recomputed in float64 by a second
  * launch; plans whose monitoring horizon extrapolates the trend past |(t - tc)/ts| = 8 run
  * float64 kernels throughout (BWM_PRECISE).  Re-entrant across streams, host threads and
- * devices: calls that use the plan's device scratch (the fixup list; the masked-mode rings of
- * large geometries) are ordered on the device through a plan-owned event, the rest overlap.
+ * devices: calls that use the plan's device scratch (the fixup list; the TMA kernel's dynamic
+ * slice-scheduler counters, which its last warp resets; the masked-mode rings of large
+ * geometries) are ordered on the device through a plan-owned event, the rest overlap.
  * zero_sigma_pixel accumulates (atomicMin) across calls until the caller re-initialises it
  * (bwm_zero_sigma_init).
  */
