@@ -677,22 +677,40 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
 #endif
             const float2* lst = st + kBox / 8;           // lag dates (kRingLag): second box
             if (t0 >= n && t0 + R <= N) {
-                float2 oldv[R], newv[R];
-                if (MODE == kRingTmem) ring_load(rb, oldv);
+                // the lagged and the new ring rows move in 8-row groups (one tcgen05.ld/st.x16 each),
+                // so a 16-date stage keeps 8 of each live, not 16: group g reads rows rb + 8g (the
+                // mirror rows cover runs past L) and writes rows wb + 8g; with h >= R no group writes
+                // a row a later group of the same stage reads
+                constexpr int G = R < 8 ? R : 8;
+                float2 oldv[G], newv[G];
                 float4 b4[R / 4];
 #pragma unroll
                 for (int q = 0; q < R / 4; ++q)
                     b4[q] = LEAN ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(s_bd + t0)[q];
                 const float* xrow = s_xt + t0 * SP;
-                float2 acck[R];                          // LEAN: MOSUM numerators of the stage
+                // LEAN: MOSUM numerators of the current 8-date group (the first-crossing search
+                // runs per group)
+                float2 acck[G];
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
                     const int t = t0 + k;
+                    if (MODE == kRingTmem && k % G == 0) {
+                        int q = rb + k;
+                        if (!MIR && q >= L) q -= L;
+                        if (k == 0) tmem_wait_st();                  // the previous stage's rows landed
+                        if (MIR || q + G <= L) {
+                            tmem_ld16(tcol(q), *reinterpret_cast<float2(*)[8]>(&oldv[0]));
+                        } else {                                     // no mirror: the run wraps
+#pragma unroll
+                            for (int g = 0; g < G; ++g) ring_ld2(q + g >= L ? q + g - L : q + g, oldv[g]);
+                            tmem_wait_ld();
+                        }
+                    }
                     const float2 r = fill(st[k * ROWF2], negc, last);
                     float2 old;
                     if (MODE == kRingTmem) {
-                        old = oldv[k];
-                        newv[k] = r;
+                        old = oldv[k % G];
+                        newv[k % G] = r;
                     } else {
                         old = fill(lst[k * ROWF2], negc, lag_last);
                     }
@@ -701,29 +719,34 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
                         // exceeds it, so the per-date test moves out of the loop (below)
                         acc = add2(acc, sub2(r, old));             // _kernels.py:33 order
                         const float2 num = wsum_row<NP, SP>(acc, xrow + k * SP, nb);
-                        acck[k] = num;
+                        acck[k % G] = num;
                         mx.x = fmaxf(mx.x, fabsf(num.x));
                         mx.y = fmaxf(mx.y, fabsf(num.y));
+                        if (k % G == G - 1) {
+                            // strict crossing (_kernels.py:47) of the group's first date past the
+                            // boundary; taken at most once per pixel
+                            const int tg = t0 + k - (G - 1) - n + 1;
+                            if (first0 == 0x7fffffff && mx.x > bsc.x) {
+#pragma unroll
+                                for (int g = G - 1; g >= 0; --g)
+                                    if (fabsf(acck[g].x) > bsc.x) first0 = tg + g;
+                            }
+                            if (first1 == 0x7fffffff && mx.y > bsc.y) {
+#pragma unroll
+                                for (int g = G - 1; g >= 0; --g)
+                                    if (fabsf(acck[g].y) > bsc.y) first1 = tg + g;
+                            }
+                        }
                     } else {
                         const float4 bq4 = b4[k >> 2];
                         step(r, old, t, (k & 3) == 0 ? bq4.x : (k & 3) == 1 ? bq4.y : (k & 3) == 2 ? bq4.z : bq4.w);
                     }
-                }
-                if (LEAN && BWM_LAZY_CROSS) {
-                    // strict crossing (_kernels.py:47) of the stage's first date past the boundary;
-                    // taken at most once per pixel
-                    if (first0 == 0x7fffffff && mx.x > bsc.x) {
-#pragma unroll
-                        for (int k = R - 1; k >= 0; --k)
-                            if (fabsf(acck[k].x) > bsc.x) first0 = t0 + k - n + 1;
-                    }
-                    if (first1 == 0x7fffffff && mx.y > bsc.y) {
-#pragma unroll
-                        for (int k = R - 1; k >= 0; --k)
-                            if (fabsf(acck[k].y) > bsc.y) first1 = t0 + k - n + 1;
+                    if (MODE == kRingTmem && k % G == G - 1) {
+                        const int q = wb + k - (G - 1);              // multiple of 8, < L
+                        tmem_st16(tcol(q), *reinterpret_cast<const float2(*)[8]>(&newv[0]));
+                        if (MIR && q < R) tmem_st16(tcol(L + q), *reinterpret_cast<const float2(*)[8]>(&newv[0]));
                     }
                 }
-                if (MODE == kRingTmem) ring_store(wb, newv);
             } else {
                 // boundary stage: dates [max(t0, n), min(t0 + R, N)), one at a time
                 if (MODE == kRingTmem) tmem_wait_st();
