@@ -1102,6 +1102,19 @@ int bwm_monitor(const bwm_plan* plan, const float* y, int64_t ld_y, int64_t n_pi
             int rc = encode_map(&kp.tmap, kp.y, cnt, d.n_obs, ld_y, bwm::kWarpPx, tall ? bwm::kTallRows : bwm::kStageRows);
             if (rc) return rc;
             kp.sched = (tall ? dyn_tall : dyn) ? plan->d_sched : nullptr;
+            {
+                // long slices (C4: 126 stages, ~170 us each): claim just in time, so the launch's last
+                // slices go to warps that are free, not to busy warps holding a pre-claimed one;
+                // short slices pre-claim one ahead (the atomic's latency would not hide)
+                const int R = tall ? bwm::kTallRows : bwm::kStageRows, n = d.n_hist, N = d.n_obs;
+                const int t3 = (n / R) * R;
+                const int ts = (n + R - 1) / R + (N - t3 + R - 1) / R;
+                static const int jit_env = [] {
+                    const char* e = std::getenv("BWM_SCHED_JIT");    // A/B: 0 never, 1 always
+                    return e ? std::atoi(e) : -1;
+                }();
+                kp.sched_jit = jit_env >= 0 ? jit_env : (ts >= 64 ? 1 : 0);
+            }
             if (tall) {
                 kp.ring_rows = plan->tring_tall.rows;
                 kp.tmem_cols = plan->tring_tall.cols;

@@ -81,6 +81,8 @@ struct KParams {
     // TMA kernel: dynamic per-warp slice scheduler ([0] claim counter, [1] finished warps; the
     // last warp to finish resets both, so every launch starts from 0) — nullptr: static schedule
     unsigned int* sched;
+    int sched_jit;              // 1: claim each slice when the cursor reaches it (long slices: no pre-claimed
+                                // slice waits behind a busy warp at the end of the launch)
 };
 
 // append pixel `px` (launch-relative) to the fixup list when its history fit is ill-conditioned:

@@ -395,7 +395,8 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
     int64_t islice = (int64_t)blockIdx.x * NW + wu;
     int64_t pending = islice;
     unsigned int pre = 0;                             // lane 0: the pre-claimed next slice (dynamic)
-    if (dyn && lane == 0) pre = atomicAdd(prm.sched, 1u);
+    const bool jit = dyn && prm.sched_jit;
+    if (dyn && !jit && lane == 0) pre = atomicAdd(prm.sched, 1u);
     int istage = 0;
     int xw = (int)(islice * kWarpPx);                 // x of the cursor's slice
     constexpr uint32_t kBox = (uint32_t)(R * kWarpPx * 4);
@@ -415,9 +416,10 @@ __global__ void __launch_bounds__(tma_threads(MODE), tma_minb(NP, MODE))
         if (++istage == tile_stages) {
             istage = 0;
             if (dyn) {
+                if (jit && lane == 0) pre = atomicAdd(prm.sched, 1u);
                 islice = n_warps + (int64_t)__shfl_sync(0xffffffffu, pre, 0);
                 if (islice < n_slices) {
-                    if (lane == 0) pre = atomicAdd(prm.sched, 1u);
+                    if (!jit && lane == 0) pre = atomicAdd(prm.sched, 1u);
                 } else if (lane == 0) {
                     // this warp's last claim; the last warp of the launch resets the scheduler
                     if (atomicAdd(prm.sched + 1, 1u) == (unsigned int)(n_warps - 1)) {
